@@ -1,0 +1,177 @@
+/*
+ * dba_b200.h — C-ABI of the B200-native dense bundle adjustment (DBA)
+ * Gauss-Newton step (DROID-Splat, arXiv 2411.17660).
+ *
+ * Drop-in boundary.  The reference package declares a `dba` module
+ * (/root/reference/pkg/src/flowsplat/__init__.py:8) whose contract is written
+ * in /root/reference/SPEC.md:286-394:
+ *
+ *   energy(problem, state) -> scalar
+ *   solve_ba(problem, state) -> state' + BAReport
+ *   solve_ba_calib(problem, state) -> state' incl. theta
+ *   energy_rgbd(problem, state, d*, alpha) -> scalar
+ *
+ * (the module file itself is absent from the reference; there is no upstream
+ * FFI, so these entry points are what a ctypes/cffi binding of that module
+ * would call — see INTEGRATION.md).  `dba_plan_create` replaces the
+ * BAProblem's graph half (edges, fixed set, block flags),
+ * `dba_solve` replaces solve_ba / solve_ba_calib (+ the prior term of
+ * energy_rgbd), `dba_energy` replaces energy / energy_rgbd, and the dba_report
+ * struct replaces BAReport.
+ *
+ * Conventions
+ *  - Ownership: the caller owns every buffer (inputs, outputs, workspace).
+ *    The library allocates only host-side plan metadata in dba_plan_create
+ *    and never allocates device memory.
+ *  - All buffer pointers in dba_buffers are DEVICE pointers; the problem
+ *    descriptor's ii/jj/fixed are HOST pointers (read once at plan creation).
+ *  - Poses: (N,7) float64 rows [qw,qx,qy,qz,tx,ty,tz], world->camera
+ *    (geometry.py:72-81).  Disparities: (N,H,W) float32.  Intrinsics:
+ *    (4,) float64 [fx,fy,cx,cy] (geometry.py:211-212).  Flow: (E_local,H,W,4)
+ *    float32 [target_u, target_v, weight_u, weight_v] — the DSPT flow record
+ *    (providers.py:12-15), rows in INPUT edge order restricted to this rank's
+ *    edges (all edges when nranks == 1).
+ *  - Errors: every entry point returns a DBA_* status; no C++ exception
+ *    crosses the ABI.  DBA_ENONFINITE sets report->bad_edge (input edge id).
+ *  - Threading: stream-ordered on `stream`; dba_solve synchronises the stream
+ *    once per Gauss-Newton trial to read the accept/reject energy.  Distinct
+ *    plans + workspaces may run concurrently on distinct streams; one plan
+ *    must not be used concurrently.
+ *  - Determinism: fixed reduction trees, no floating-point atomics; results
+ *    are bitwise reproducible for a fixed plan (rank count, split count).
+ */
+#ifndef DBA_B200_H_
+#define DBA_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DBA_VERSION 1
+
+/* status codes -> flowsplat.errors (errors.py:8-29) */
+#define DBA_OK 0
+#define DBA_EINVAL 1       /* ValueError / ConfigError */
+#define DBA_ECAPACITY 2    /* CapacityError (compiled limits) */
+#define DBA_ENONFINITE 3   /* NumericalError, report->bad_edge */
+#define DBA_ESOLVER 4      /* SolverFailure */
+#define DBA_ECALIB 5       /* CalibrationDegenerateError */
+#define DBA_ECUDA 6        /* CUDA runtime failure */
+#define DBA_ENCCL 7        /* NCCL failure */
+
+#define DBA_TRACE_MAX 64
+
+typedef struct dba_plan dba_plan;
+
+/* Graph half of SPEC BAProblem. */
+typedef struct {
+  int32_t n_frames;            /* N */
+  int32_t height, width;       /* H, W (the 1/8-resolution BA grid) */
+  int32_t n_edges;             /* E (global) */
+  const int32_t* ii;           /* host (E,) source frame per edge */
+  const int32_t* jj;           /* host (E,) target frame per edge */
+  const uint8_t* fixed;        /* host (N,) 1 = pose held fixed (gauge) */
+  int32_t optimize_intrinsics; /* solve_ba_calib */
+  int32_t use_prior;           /* energy_rgbd term */
+  int32_t scale_gauge;         /* -1 auto (1 fixed pose, no prior), 0 off, 1 on */
+  int32_t rank, nranks;        /* edge sharding by source frame */
+} dba_problem_desc;
+
+/* Solver knobs. */
+typedef struct {
+  int32_t iters;        /* accepted GN iterations budget (4 frontend, 8 backend) */
+  double lambda0;       /* initial damping on the reduced pose system */
+  double lambda_min;    /* floor after an accepted step (lambda /= 10) */
+  double lambda_max;    /* rejects beyond this stop the solve */
+  double eta;           /* disparity-diagonal damping */
+  double alpha;         /* prior weight (1e-3) */
+  double d_min;         /* disparity floor (1e-6) */
+  double tangent_max;   /* per-pose tangent clamp (1) */
+  double calib_cond_max;/* A9 degeneracy threshold */
+} dba_options;
+
+typedef struct {
+  const double* poses_in;   /* (N,7) */
+  double* poses_out;        /* (N,7) */
+  const float* disps_in;    /* (N,H,W) */
+  float* disps_out;         /* (N,H,W) (only this rank's frames are written) */
+  const double* intr_in;    /* (4,) */
+  double* intr_out;         /* (4,) */
+  const float* flow;        /* (E_local,H,W,4) */
+  const float* prior;       /* (N,H,W) or NULL */
+  const uint8_t* prior_mask;/* (N,H,W) or NULL */
+  void* workspace;          /* >= dba_plan_workspace_bytes, 256-byte aligned */
+  size_t workspace_bytes;
+  void* stream;             /* cudaStream_t (NULL = legacy default stream) */
+  void* nccl_comm;          /* ncclComm_t for nranks > 1, else NULL */
+} dba_buffers;
+
+/* SPEC BAReport + diagnostics. */
+typedef struct {
+  int32_t status;
+  int32_t bad_edge;         /* input edge id for DBA_ENONFINITE, else -1 */
+  int32_t iterations;       /* accepted GN iterations */
+  int32_t trials;           /* linearize+solve+back-substitute passes after the first */
+  int32_t converged;        /* 1 if the damping schedule ran out without a decrease */
+  int32_t trace_len;
+  double initial_energy;
+  double final_energy;
+  double lambda_final;
+  double scale;             /* mono gauge factor applied at the end (1 if off) */
+  double calib_condition;   /* A9 estimate of the last solve (0 if not calibrating) */
+  double energy_trace[DBA_TRACE_MAX];
+} dba_report;
+
+typedef struct {
+  int32_t n_reduced;        /* size of the reduced pose(+theta) system */
+  int32_t n_free_poses;
+  int32_t band_blocks;      /* block bandwidth BW of the reduced system */
+  int32_t frame_begin, frame_end;   /* this rank's source frames */
+  int32_t n_local_edges;
+  int32_t max_out_degree;
+  int32_t n_split;          /* pixel splits per frame in the fused pass */
+  int32_t gauge_frame;      /* -1 when the scale gauge is off */
+  int64_t workspace_bytes;
+} dba_plan_info;
+
+int dba_version(void);
+const char* dba_status_string(int status);
+
+/* Frame partition used for edge sharding: contiguous source-frame ranges with
+ * balanced (out-degree + 1) weight.  bounds: (nranks+1,) host output. */
+int dba_partition(int32_t n_frames, int32_t n_edges, const int32_t* ii, int32_t nranks,
+                  int32_t* bounds);
+
+int dba_plan_create(const dba_problem_desc* desc, dba_plan** out);
+void dba_plan_destroy(dba_plan* plan);
+int dba_plan_get_info(const dba_plan* plan, dba_plan_info* info);
+/* (E_local,) host output: input edge id of each local flow row. */
+int dba_plan_local_edges(const dba_plan* plan, int32_t* edge_ids);
+
+/* solve_ba / solve_ba_calib: damped Gauss-Newton with Schur elimination. */
+int dba_solve(dba_plan* plan, const dba_options* opt, const dba_buffers* buf,
+              dba_report* report);
+
+/* energy / energy_rgbd at the input state (poses_in, disps_in, intr_in). */
+int dba_energy(dba_plan* plan, const dba_options* opt, const dba_buffers* buf,
+               double* energy);
+
+/* Test hook: the Schur-reduced system at the input state, expanded to a dense
+ * host (n_reduced x n_reduced) matrix + host rhs (n_reduced,) + energy.  With
+ * nccl_comm == NULL and nranks > 1 this is this rank's PARTIAL system. */
+int dba_build_system(dba_plan* plan, const dba_options* opt, const dba_buffers* buf,
+                     double* S_host, double* y_host, double* energy);
+
+/* NCCL bootstrap helpers (the library links NCCL; ids travel as 128 bytes). */
+int dba_nccl_unique_id(uint8_t id_out[128]);
+int dba_nccl_comm_init(int32_t nranks, const uint8_t id[128], int32_t rank, void** comm_out);
+int dba_nccl_comm_destroy(void* comm);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DBA_B200_H_ */

@@ -1,0 +1,1016 @@
+// Host side of libdba_b200: plan construction (graph -> CSR, frame partition,
+// band structure, deterministic assembly lists, workspace layout), the damped
+// Gauss-Newton loop and the C-ABI declared in include/dba_b200.h.
+//
+// One GN trial = solve (K3b) -> prep (K4) -> pass (K1+K2+K3a+K5, back-substitution
+// fused) -> assemble -> gather -> finalize [-> ncclAllReduce of the packed
+// reduced system] -> one 32-byte device->host read for accept/reject
+// (SPEC.md:375).  The reference SPEC contract is SPEC.md:286-394.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <set>
+#include <utility>
+#include <vector>
+
+#include "../../include/dba_b200.h"
+#include "dba_common.cuh"
+#include "dba_pass.cuh"
+#include "dba_solve.cuh"
+#include "dba_system.cuh"
+
+using namespace dba;
+
+namespace {
+
+// NCCL is resolved at run time from the process (torch already loads its own
+// libnccl.so.2); the library has no link-time NCCL dependency, so it never
+// drags a second NCCL build into the process.
+struct NcclApi {
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  bool ok = false;
+};
+
+const NcclApi& nccl() {
+  static NcclApi api = [] {
+    NcclApi a;
+    void* h = RTLD_DEFAULT;
+    if (!dlsym(h, "ncclAllReduce")) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return a;
+    a.GetUniqueId = reinterpret_cast<decltype(a.GetUniqueId)>(dlsym(h, "ncclGetUniqueId"));
+    a.CommInitRank = reinterpret_cast<decltype(a.CommInitRank)>(dlsym(h, "ncclCommInitRank"));
+    a.CommDestroy = reinterpret_cast<decltype(a.CommDestroy)>(dlsym(h, "ncclCommDestroy"));
+    a.AllReduce = reinterpret_cast<decltype(a.AllReduce)>(dlsym(h, "ncclAllReduce"));
+    a.ok = a.GetUniqueId && a.CommInitRank && a.CommDestroy && a.AllReduce;
+    return a;
+  }();
+  return api;
+}
+
+constexpr size_t kAlign = 256;
+inline size_t align_up(size_t x) { return (x + kAlign - 1) & ~(kAlign - 1); }
+
+struct Readback {
+  int status[4];  // [0] factorisation failed, [1] bad edge (INT_MAX = none)
+  double cond;
+  double energy;
+  double pad[2];
+};
+
+struct Layout {
+  // metadata (uploaded once per workspace)
+  size_t csr_off, slot_flow, frame_of, slot_i, slot_j, slot_edge, ridx;
+  size_t seg_frame, seg_t0, seg_t1, seg_off_edge, seg_off_M, seg_off_w, cta_seg, frame_seg;
+  size_t off_F, off_f, units, contrib, meta_end;
+  // state
+  size_t poses[2], intr[2], disps[2], xi, delta, lin, back, adj;
+  size_t part_edge, part_M, part_w, part_frame, Fbuf, sys[2], Lband, flags, gauge, total;
+};
+
+}  // namespace
+
+struct dba_plan {
+  int N = 0, H = 0, W = 0, P = 0, E = 0;
+  int calib = 0, prior = 0, gauge_on = 0, gauge_frame = -1, rank = 0, nranks = 1;
+  int f0 = 0, f1 = 0, NL = 0, EL = 0, kmax = 0, nb = 0, BW = 0, n_red = 0;
+  int n_tiles = 0, G = 0, nseg = 0, n_units = 0, nve = kEdgeVals, MT = 1;
+  size_t pass_smem = 0, solve_smem = 0;
+  long long sys_len = 0;  // doubles in one packed reduced system
+  long long band_len = 0, theta_off = 0, thth_off = 0, y_off = 0, energy_off = 0;
+  std::vector<int> fixed_ridx;
+  std::vector<int> local_edges;  // input edge id of each local flow row
+  Layout L{};
+  std::vector<unsigned char> meta;  // image of [0, meta_end)
+  unsigned char* meta_pinned = nullptr;
+  Readback* rb = nullptr;
+  const void* uploaded_ws = nullptr;
+  int device = -1;
+};
+
+namespace {
+
+template <typename T>
+void put(std::vector<unsigned char>& img, size_t off, const std::vector<T>& v) {
+  if (!v.empty()) std::memcpy(img.data() + off, v.data(), sizeof(T) * v.size());
+}
+
+int cuda_status(cudaError_t e) {
+  if (e == cudaSuccess) return DBA_OK;
+  fprintf(stderr, "libdba_b200: CUDA error %s\n", cudaGetErrorString(e));
+  return DBA_ECUDA;
+}
+
+#define DBA_CUDA(x)                                \
+  do {                                             \
+    int _s = cuda_status((x));                     \
+    if (_s != DBA_OK) return _s;                   \
+  } while (0)
+
+int partition_frames(int N, int E, const int32_t* ii, int R, std::vector<int>& bounds) {
+  if (N < 1 || R < 1 || E < 0) return DBA_EINVAL;
+  std::vector<long long> w(N, 1);
+  for (int e = 0; e < E; ++e) {
+    if (ii[e] < 0 || ii[e] >= N) return DBA_EINVAL;
+    w[ii[e]] += 1;
+  }
+  std::vector<long long> pre(N + 1, 0);
+  for (int f = 0; f < N; ++f) pre[f + 1] = pre[f] + w[f];
+  const long long tot = pre[N];
+  bounds.assign(R + 1, 0);
+  bounds[R] = N;
+  for (int r = 1; r < R; ++r) {
+    int f = 0;
+    while (f < N && pre[f] * R < (long long)r * tot) ++f;
+    bounds[r] = std::max(f, bounds[r - 1]);
+  }
+  return DBA_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int dba_version(void) { return DBA_VERSION; }
+
+const char* dba_status_string(int s) {
+  switch (s) {
+    case DBA_OK: return "ok";
+    case DBA_EINVAL: return "invalid argument";
+    case DBA_ECAPACITY: return "compiled capacity exceeded";
+    case DBA_ENONFINITE: return "non-finite residuals";
+    case DBA_ESOLVER: return "reduced system singular at maximum damping";
+    case DBA_ECALIB: return "intrinsics degenerate (poorly conditioned)";
+    case DBA_ECUDA: return "CUDA error";
+    case DBA_ENCCL: return "NCCL error";
+    default: return "unknown status";
+  }
+}
+
+int dba_partition(int32_t n_frames, int32_t n_edges, const int32_t* ii, int32_t nranks,
+                  int32_t* bounds) {
+  if (!ii || !bounds) return DBA_EINVAL;
+  std::vector<int> b;
+  int s = partition_frames(n_frames, n_edges, ii, nranks, b);
+  if (s != DBA_OK) return s;
+  for (int r = 0; r <= nranks; ++r) bounds[r] = b[r];
+  return DBA_OK;
+}
+
+int dba_plan_create(const dba_problem_desc* d, dba_plan** out) {
+  if (!d || !out || !d->ii || !d->jj || !d->fixed) return DBA_EINVAL;
+  *out = nullptr;
+  const int N = d->n_frames, E = d->n_edges;
+  if (N < 2 || E < 1 || d->height < 1 || d->width < 1) return DBA_EINVAL;
+  if (d->nranks < 1 || d->rank < 0 || d->rank >= d->nranks) return DBA_EINVAL;
+  std::set<std::pair<int, int>> seen;
+  for (int e = 0; e < E; ++e) {
+    const int i = d->ii[e], j = d->jj[e];
+    if (i < 0 || i >= N || j < 0 || j >= N || i == j) return DBA_EINVAL;
+    if (!seen.insert({i, j}).second) return DBA_EINVAL;  // FrameGraph is a set
+  }
+  int nfixed = 0;
+  for (int k = 0; k < N; ++k) nfixed += d->fixed[k] ? 1 : 0;
+  if (nfixed < 1) return DBA_EINVAL;  // gauge anchor
+
+  dba_plan* p = new (std::nothrow) dba_plan();
+  if (!p) return DBA_ECAPACITY;
+  p->N = N;
+  p->H = d->height;
+  p->W = d->width;
+  p->P = d->height * d->width;
+  p->E = E;
+  p->calib = d->optimize_intrinsics ? 1 : 0;
+  p->prior = d->use_prior ? 1 : 0;
+  p->rank = d->rank;
+  p->nranks = d->nranks;
+  p->nve = kEdgeVals + (p->calib ? kCalibVals : 0);
+  int gauge = d->scale_gauge;
+  if (gauge < 0) gauge = (nfixed == 1 && !p->prior) ? 1 : 0;
+  p->gauge_on = gauge;
+  for (int k = 0; k < N && p->gauge_frame < 0; ++k)
+    if (d->fixed[k]) p->gauge_frame = k;
+  if (!gauge) p->gauge_frame = -1;
+
+  // ---- partition + local CSR (stable by source frame)
+  std::vector<int> bounds;
+  int st = partition_frames(N, E, d->ii, d->nranks, bounds);
+  if (st != DBA_OK) {
+    delete p;
+    return st;
+  }
+  p->f0 = bounds[d->rank];
+  p->f1 = bounds[d->rank + 1];
+  p->NL = p->f1 - p->f0;
+  std::vector<int> local_rank_of_edge(E, -1);
+  for (int e = 0; e < E; ++e)
+    if (d->ii[e] >= p->f0 && d->ii[e] < p->f1) {
+      local_rank_of_edge[e] = (int)p->local_edges.size();
+      p->local_edges.push_back(e);
+    }
+  p->EL = (int)p->local_edges.size();
+  std::vector<int> csr_off(p->NL + 1, 0), slot_flow, slot_i, slot_j, slot_edge, frame_of(p->NL);
+  for (int fl = 0; fl < p->NL; ++fl) {
+    frame_of[fl] = p->f0 + fl;
+    for (int e : p->local_edges)
+      if (d->ii[e] == p->f0 + fl) {
+        slot_flow.push_back(local_rank_of_edge[e]);
+        slot_i.push_back(d->ii[e]);
+        slot_j.push_back(d->jj[e]);
+        slot_edge.push_back(e);
+      }
+    csr_off[fl + 1] = (int)slot_flow.size();
+    p->kmax = std::max(p->kmax, csr_off[fl + 1] - csr_off[fl]);
+  }
+  // out-degree limit over ALL frames (the structure is replicated)
+  {
+    std::vector<int> deg(N, 0);
+    for (int e = 0; e < E; ++e) deg[d->ii[e]]++;
+    for (int k = 0; k < N; ++k)
+      if (deg[k] > kMaxOutDegree) {
+        delete p;
+        return DBA_ECAPACITY;
+      }
+  }
+
+  // ---- reduced variables: free poses in index order, theta last
+  p->fixed_ridx.assign(N, -1);
+  int nfree = 0;
+  for (int k = 0; k < N; ++k)
+    if (!d->fixed[k]) p->fixed_ridx[k] = nfree++;
+  p->nb = nfree;
+  p->n_red = 6 * nfree + 4 * p->calib;
+  // band width from the fill-in pattern of every source frame
+  std::vector<std::vector<int>> vars(N);
+  for (int k = 0; k < N; ++k) vars[k].push_back(k);
+  {
+    std::vector<int> order(E);
+    for (int e = 0; e < E; ++e) order[e] = e;
+    std::stable_sort(order.begin(), order.end(),
+                     [&](int a, int b) { return d->ii[a] < d->ii[b]; });
+    for (int e : order) vars[d->ii[e]].push_back(d->jj[e]);
+  }
+  int BW = 0;
+  for (int k = 0; k < N; ++k)
+    for (int a : vars[k])
+      for (int c : vars[k]) {
+        const int ra = p->fixed_ridx[a], rc = p->fixed_ridx[c];
+        if (ra >= 0 && rc >= 0) BW = std::max(BW, std::abs(ra - rc));
+      }
+  p->BW = (p->nb > 0) ? std::min(BW, p->nb - 1) : 0;
+  const int W1 = p->BW + 1;
+  p->band_len = (long long)p->nb * W1 * 36;
+  p->theta_off = p->band_len;
+  p->thth_off = p->theta_off + (long long)p->nb * 24;
+  p->y_off = p->thth_off + 16;
+  p->energy_off = p->y_off + p->n_red;
+  p->sys_len = (p->energy_off + 1 + 3) & ~3LL;
+
+  // ---- solve kernel shared memory
+  {
+    const SolveSmem s = solve_smem_layout(p->nb, p->BW, p->calib);
+    p->solve_smem = s.total;
+    if (p->solve_smem > 200 * 1024) {
+      delete p;
+      return DBA_ECAPACITY;
+    }
+  }
+
+  // ---- pass decomposition: G CTAs over (frame, 256-px tile) work items
+  p->n_tiles = (p->P + kBlock - 1) / kBlock;
+  {
+    const PassSmem s = pass_smem_layout(std::max(p->kmax, 1), p->calib);
+    p->pass_smem = s.total;
+    const int mpad = pass_mpad(std::max(p->kmax, 1), p->calib);
+    const int nt = mpad / 4, ntiles = nt * (nt + 1) / 2;
+    p->MT = ntiles <= kBlock ? 1 : (ntiles <= 2 * kBlock ? 2 : 4);
+    if (p->pass_smem > 220 * 1024 || p->MT > 2) {
+      delete p;
+      return DBA_ECAPACITY;
+    }
+  }
+  int dev = 0, sms = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) {
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, dev) == cudaSuccess) sms = prop.multiProcessorCount;
+  }
+  p->device = dev;
+  const int per_sm = std::max(1, std::min(2, (int)((227 * 1024) / std::max<size_t>(p->pass_smem, 1))));
+  const long long items = (long long)p->NL * p->n_tiles;
+  p->G = (int)std::max<long long>(1, std::min<long long>(items, (long long)sms * per_sm));
+  // weighted contiguous split, cost of a tile ~ (out-degree + 2)
+  std::vector<int> seg_frame, seg_t0, seg_t1, cta_seg(p->G + 1, 0), frame_seg(p->NL + 1, 0);
+  {
+    long long tot = 0;
+    for (int fl = 0; fl < p->NL; ++fl)
+      tot += (long long)(csr_off[fl + 1] - csr_off[fl] + 2) * p->n_tiles;
+    long long cum = 0;
+    int cur_cta = -1, cur_fl = -1;
+    for (int fl = 0; fl < p->NL; ++fl) {
+      const long long c = csr_off[fl + 1] - csr_off[fl] + 2;
+      for (int t = 0; t < p->n_tiles; ++t) {
+        int cta = (int)std::min<long long>(p->G - 1, ((2 * cum + c) * p->G) / (2 * std::max(tot, 1LL)));
+        cta = std::max(cta, std::max(cur_cta, 0));
+        if (cta != cur_cta || fl != cur_fl) {
+          while (cur_cta < cta) cta_seg[++cur_cta] = (int)seg_frame.size();
+          seg_frame.push_back(fl);
+          seg_t0.push_back(t);
+          seg_t1.push_back(t + 1);
+          cur_fl = fl;
+        } else {
+          seg_t1.back() = t + 1;
+        }
+        cum += c;
+      }
+    }
+    while (cur_cta < p->G) cta_seg[++cur_cta] = (int)seg_frame.size();
+    cta_seg[p->G] = (int)seg_frame.size();
+    p->nseg = (int)seg_frame.size();
+    for (int s = 0; s < p->nseg; ++s) frame_seg[seg_frame[s] + 1] = s + 1;
+    for (int fl = 0; fl < p->NL; ++fl) frame_seg[fl + 1] = std::max(frame_seg[fl + 1], frame_seg[fl]);
+  }
+  std::vector<long long> seg_off_edge(p->nseg), seg_off_M(p->nseg), seg_off_w(p->nseg);
+  long long n_pe = 0, n_pM = 0, n_pw = 0;
+  for (int s = 0; s < p->nseg; ++s) {
+    const int fl = seg_frame[s];
+    const int k = csr_off[fl + 1] - csr_off[fl];
+    const int mu = pass_mu(k, p->calib);
+    seg_off_edge[s] = n_pe;
+    seg_off_M[s] = n_pM;
+    seg_off_w[s] = n_pw;
+    n_pe += (long long)k * p->nve;
+    n_pM += (long long)mu * mu;
+    n_pw += mu;
+  }
+  // frame factors
+  std::vector<long long> off_F(p->NL), off_f(p->NL);
+  long long nF = 0;
+  for (int fl = 0; fl < p->NL; ++fl) {
+    const int k = csr_off[fl + 1] - csr_off[fl];
+    const int m = k > 0 ? 6 * (k + 1) + 4 * p->calib : 0;
+    off_F[fl] = nF;
+    nF += (long long)m * m;
+    off_f[fl] = nF;
+    nF += m;
+  }
+
+  // ---- deterministic gather lists for the packed reduced system
+  std::vector<GatherUnit> units;
+  std::vector<Contrib> contrib;
+  {
+    // per local frame: local block row start of a global pose / theta
+    auto local_row = [&](int fl, int pose) -> int {
+      const int s0 = csr_off[fl], k = csr_off[fl + 1] - s0;
+      if (pose == p->f0 + fl) return 0;
+      for (int a = 0; a < k; ++a)
+        if (slot_j[s0 + a] == pose) return 6 * (a + 1);
+      return -1;
+    };
+    auto mdim = [&](int fl) {
+      const int k = csr_off[fl + 1] - csr_off[fl];
+      return k > 0 ? 6 * (k + 1) + 4 * p->calib : 0;
+    };
+    std::vector<int> pose_of_block(p->nb);
+    for (int k = 0; k < N; ++k)
+      if (p->fixed_ridx[k] >= 0) pose_of_block[p->fixed_ridx[k]] = k;
+    // band blocks
+    for (int a = 0; a < p->nb; ++a)
+      for (int pos = 0; pos < W1; ++pos) {
+        const int c = a - p->BW + pos;
+        GatherUnit u;
+        u.dst = ((long long)a * W1 + pos) * 36;
+        u.rows = 6;
+        u.cols = 6;
+        u.c0 = (int)contrib.size();
+        if (c >= 0) {
+          const int pa = pose_of_block[a], pc = pose_of_block[c];
+          for (int fl = 0; fl < p->NL; ++fl) {
+            const int m = mdim(fl);
+            if (m == 0) continue;
+            const int ra = local_row(fl, pa), rc = local_row(fl, pc);
+            if (ra < 0 || rc < 0) continue;
+            contrib.push_back({off_F[fl] + (long long)ra * m + rc, m, 0});
+          }
+        }
+        u.c1 = (int)contrib.size();
+        units.push_back(u);
+      }
+    if (p->calib) {
+      for (int c = 0; c < p->nb; ++c) {
+        GatherUnit u;
+        u.dst = p->theta_off + (long long)c * 24;
+        u.rows = 4;
+        u.cols = 6;
+        u.c0 = (int)contrib.size();
+        const int pc = pose_of_block[c];
+        for (int fl = 0; fl < p->NL; ++fl) {
+          const int m = mdim(fl);
+          if (m == 0) continue;
+          const int rc = local_row(fl, pc);
+          if (rc < 0) continue;
+          contrib.push_back({off_F[fl] + (long long)(m - 4) * m + rc, m, 0});
+        }
+        u.c1 = (int)contrib.size();
+        units.push_back(u);
+      }
+      GatherUnit u;
+      u.dst = p->thth_off;
+      u.rows = 4;
+      u.cols = 4;
+      u.c0 = (int)contrib.size();
+      for (int fl = 0; fl < p->NL; ++fl) {
+        const int m = mdim(fl);
+        if (m == 0) continue;
+        contrib.push_back({off_F[fl] + (long long)(m - 4) * m + (m - 4), m, 0});
+      }
+      u.c1 = (int)contrib.size();
+      units.push_back(u);
+    }
+    // right-hand side
+    for (int a = 0; a < p->nb; ++a) {
+      GatherUnit u;
+      u.dst = p->y_off + 6LL * a;
+      u.rows = 6;
+      u.cols = 1;
+      u.c0 = (int)contrib.size();
+      for (int fl = 0; fl < p->NL; ++fl) {
+        const int m = mdim(fl);
+        if (m == 0) continue;
+        const int ra = local_row(fl, pose_of_block[a]);
+        if (ra < 0) continue;
+        contrib.push_back({off_f[fl] + ra, 1, 0});
+      }
+      u.c1 = (int)contrib.size();
+      units.push_back(u);
+    }
+    if (p->calib) {
+      GatherUnit u;
+      u.dst = p->y_off + 6LL * p->nb;
+      u.rows = 4;
+      u.cols = 1;
+      u.c0 = (int)contrib.size();
+      for (int fl = 0; fl < p->NL; ++fl) {
+        const int m = mdim(fl);
+        if (m == 0) continue;
+        contrib.push_back({off_f[fl] + (m - 4), 1, 0});
+      }
+      u.c1 = (int)contrib.size();
+      units.push_back(u);
+    }
+  }
+  p->n_units = (int)units.size();
+
+  // ---- workspace layout
+  Layout& L = p->L;
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    const size_t r = o;
+    o = align_up(o + std::max<size_t>(bytes, 1));
+    return r;
+  };
+  L.csr_off = take(sizeof(int) * csr_off.size());
+  L.slot_flow = take(sizeof(int) * slot_flow.size());
+  L.frame_of = take(sizeof(int) * frame_of.size());
+  L.slot_i = take(sizeof(int) * slot_i.size());
+  L.slot_j = take(sizeof(int) * slot_j.size());
+  L.slot_edge = take(sizeof(int) * slot_edge.size());
+  L.ridx = take(sizeof(int) * N);
+  L.seg_frame = take(sizeof(int) * seg_frame.size());
+  L.seg_t0 = take(sizeof(int) * seg_t0.size());
+  L.seg_t1 = take(sizeof(int) * seg_t1.size());
+  L.seg_off_edge = take(sizeof(long long) * p->nseg);
+  L.seg_off_M = take(sizeof(long long) * p->nseg);
+  L.seg_off_w = take(sizeof(long long) * p->nseg);
+  L.cta_seg = take(sizeof(int) * cta_seg.size());
+  L.frame_seg = take(sizeof(int) * frame_seg.size());
+  L.off_F = take(sizeof(long long) * off_F.size());
+  L.off_f = take(sizeof(long long) * off_f.size());
+  L.units = take(sizeof(GatherUnit) * units.size());
+  L.contrib = take(sizeof(Contrib) * contrib.size());
+  L.meta_end = o;
+  for (int s = 0; s < 2; ++s) {
+    L.poses[s] = take(sizeof(double) * 7 * N);
+    L.intr[s] = take(sizeof(double) * 4);
+    L.disps[s] = take(sizeof(float) * (size_t)N * p->P);
+    L.sys[s] = take(sizeof(double) * p->sys_len);
+  }
+  L.xi = take(sizeof(double) * 6 * N);
+  L.delta = take(sizeof(double) * (p->n_red + 4));
+  L.lin = take(sizeof(EdgeLin) * p->EL);
+  L.back = take(sizeof(EdgeBack) * p->EL);
+  L.adj = take(sizeof(double) * 36 * (size_t)p->EL);
+  L.part_edge = take(sizeof(double) * n_pe);
+  L.part_M = take(sizeof(double) * n_pM);
+  L.part_w = take(sizeof(double) * n_pw);
+  L.part_frame = take(sizeof(double) * kFrameVals * (size_t)p->nseg);
+  L.Fbuf = take(sizeof(double) * nF);
+  L.Lband = take(sizeof(double) * std::max<long long>(p->band_len, 1));
+  L.flags = take(sizeof(Readback));
+  L.gauge = take(sizeof(double) * 4);
+  L.total = o;
+
+  p->meta.assign(L.meta_end, 0);
+  put(p->meta, L.csr_off, csr_off);
+  put(p->meta, L.slot_flow, slot_flow);
+  put(p->meta, L.frame_of, frame_of);
+  put(p->meta, L.slot_i, slot_i);
+  put(p->meta, L.slot_j, slot_j);
+  put(p->meta, L.slot_edge, slot_edge);
+  put(p->meta, L.ridx, p->fixed_ridx);
+  put(p->meta, L.seg_frame, seg_frame);
+  put(p->meta, L.seg_t0, seg_t0);
+  put(p->meta, L.seg_t1, seg_t1);
+  put(p->meta, L.seg_off_edge, seg_off_edge);
+  put(p->meta, L.seg_off_M, seg_off_M);
+  put(p->meta, L.seg_off_w, seg_off_w);
+  put(p->meta, L.cta_seg, cta_seg);
+  put(p->meta, L.frame_seg, frame_seg);
+  put(p->meta, L.off_F, off_F);
+  put(p->meta, L.off_f, off_f);
+  put(p->meta, L.units, units);
+  put(p->meta, L.contrib, contrib);
+  *out = p;
+  return DBA_OK;
+}
+
+void dba_plan_destroy(dba_plan* p) {
+  if (!p) return;
+  if (p->meta_pinned) cudaFreeHost(p->meta_pinned);
+  if (p->rb) cudaFreeHost(p->rb);
+  delete p;
+}
+
+int dba_plan_get_info(const dba_plan* p, dba_plan_info* info) {
+  if (!p || !info) return DBA_EINVAL;
+  info->n_reduced = p->n_red;
+  info->n_free_poses = p->nb;
+  info->band_blocks = p->BW;
+  info->frame_begin = p->f0;
+  info->frame_end = p->f1;
+  info->n_local_edges = p->EL;
+  info->max_out_degree = p->kmax;
+  info->n_split = p->G;
+  info->gauge_frame = p->gauge_frame;
+  info->workspace_bytes = (int64_t)p->L.total;
+  return DBA_OK;
+}
+
+int dba_plan_local_edges(const dba_plan* p, int32_t* ids) {
+  if (!p || !ids) return DBA_EINVAL;
+  for (int s = 0; s < p->EL; ++s) ids[s] = p->local_edges[s];
+  return DBA_OK;
+}
+
+}  // extern "C"
+
+// ============================================================== execution
+
+namespace {
+
+struct Ctx {
+  dba_plan* p;
+  const dba_options* o;
+  const dba_buffers* b;
+  cudaStream_t st;
+  unsigned char* ws;
+  ncclComm_t comm;
+  template <typename T>
+  T* at(size_t off) const {
+    return reinterpret_cast<T*>(ws + off);
+  }
+};
+
+int check_args(dba_plan* p, const dba_options* o, const dba_buffers* b) {
+  if (!p || !o || !b) return DBA_EINVAL;
+  if (!b->poses_in || !b->disps_in || !b->intr_in || !b->workspace) return DBA_EINVAL;
+  if (p->EL > 0 && !b->flow) return DBA_EINVAL;
+  if (b->workspace_bytes < p->L.total) return DBA_EINVAL;
+  if ((reinterpret_cast<uintptr_t>(b->workspace) & (kAlign - 1)) != 0) return DBA_EINVAL;
+  if (p->prior && (!b->prior || !b->prior_mask)) return DBA_EINVAL;
+  if (p->nranks > 1 && !b->nccl_comm) {
+    // allowed only for dba_build_system (partial systems); dba_solve checks itself
+  }
+  if (!(o->eta > 0.0) || !(o->lambda0 > 0.0) || o->iters < 0) return DBA_EINVAL;
+  return DBA_OK;
+}
+
+int prepare(Ctx& c) {
+  dba_plan* p = c.p;
+  if (!p->meta_pinned) {
+    DBA_CUDA(cudaMallocHost(&p->meta_pinned, std::max<size_t>(p->meta.size(), 1)));
+    std::memcpy(p->meta_pinned, p->meta.data(), p->meta.size());
+    DBA_CUDA(cudaMallocHost(&p->rb, sizeof(Readback)));
+  }
+  if (p->uploaded_ws != c.b->workspace) {
+    DBA_CUDA(cudaMemcpyAsync(c.ws, p->meta_pinned, p->meta.size(), cudaMemcpyHostToDevice, c.st));
+    p->uploaded_ws = c.b->workspace;
+  }
+  return DBA_OK;
+}
+
+int launch_prep(Ctx& c, int cur, int nxt, bool init) {
+  dba_plan* p = c.p;
+  PrepArgs a;
+  a.N = p->N;
+  a.EL = p->EL;
+  a.init = init ? 1 : 0;
+  a.calib = p->calib;
+  a.theta_off = 6 * p->nb;
+  a.tmax = c.o->tangent_max;
+  a.status = c.at<int>(p->L.flags);
+  a.ridx = c.at<int>(p->L.ridx);
+  a.slot_i = c.at<int>(p->L.slot_i);
+  a.slot_j = c.at<int>(p->L.slot_j);
+  a.poses_c = c.at<double>(p->L.poses[cur]);
+  a.poses_n = c.at<double>(p->L.poses[nxt]);
+  a.intr_c = c.at<double>(p->L.intr[cur]);
+  a.intr_n = c.at<double>(p->L.intr[nxt]);
+  a.delta = c.at<double>(p->L.delta);
+  a.xi_out = c.at<double>(p->L.xi);
+  a.lin = c.at<EdgeLin>(p->L.lin);
+  a.back = c.at<EdgeBack>(p->L.back);
+  a.adj = c.at<double>(p->L.adj);
+  const int n = p->N + p->EL + 1;
+  prep_kernel<<<(n + 127) / 128, 128, 0, c.st>>>(a);
+  return cuda_status(cudaGetLastError());
+}
+
+template <bool CALIB, int MT>
+int launch_pass_t(Ctx& c, const PassArgs& a) {
+  auto k = pass_kernel<CALIB, MT>;
+  DBA_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.p->pass_smem));
+  k<<<c.p->G, kBlock, c.p->pass_smem, c.st>>>(a);
+  return cuda_status(cudaGetLastError());
+}
+
+int launch_pass(Ctx& c, int cur, int nxt, bool backsub, bool system) {
+  dba_plan* p = c.p;
+  if (p->NL == 0) return DBA_OK;
+  PassArgs a;
+  a.H = p->H;
+  a.W = p->W;
+  a.P = p->P;
+  a.n_tiles = p->n_tiles;
+  a.kmax = std::max(p->kmax, 1);
+  a.backsub = backsub ? 1 : 0;
+  a.system = system ? 1 : 0;
+  a.status = c.at<int>(p->L.flags);
+  a.csr_off = c.at<int>(p->L.csr_off);
+  a.slot_flow = c.at<int>(p->L.slot_flow);
+  a.frame_of = c.at<int>(p->L.frame_of);
+  a.seg_frame = c.at<int>(p->L.seg_frame);
+  a.seg_t0 = c.at<int>(p->L.seg_t0);
+  a.seg_t1 = c.at<int>(p->L.seg_t1);
+  a.cta_seg = c.at<int>(p->L.cta_seg);
+  a.lin = c.at<EdgeLin>(p->L.lin);
+  a.back = c.at<EdgeBack>(p->L.back);
+  a.flow = reinterpret_cast<const float4*>(c.b->flow);
+  a.d_cur = c.at<float>(p->L.disps[cur]);
+  a.d_new = c.at<float>(p->L.disps[nxt]);
+  a.prior = p->prior ? c.b->prior : nullptr;
+  a.pmask = p->prior ? c.b->prior_mask : nullptr;
+  a.alpha = (float)c.o->alpha;
+  a.eta = (float)c.o->eta;
+  a.d_min = (float)c.o->d_min;
+  a.intr_c = c.at<double>(p->L.intr[cur]);
+  a.intr_n = c.at<double>(p->L.intr[nxt]);
+  a.part_edge = c.at<double>(p->L.part_edge);
+  a.part_M = c.at<double>(p->L.part_M);
+  a.part_w = c.at<double>(p->L.part_w);
+  a.part_frame = c.at<double>(p->L.part_frame);
+  a.seg_off_edge = c.at<long long>(p->L.seg_off_edge);
+  a.seg_off_M = c.at<long long>(p->L.seg_off_M);
+  a.seg_off_w = c.at<long long>(p->L.seg_off_w);
+  if (p->calib) {
+    if (p->MT == 1) return launch_pass_t<true, 1>(c, a);
+    return launch_pass_t<true, 2>(c, a);
+  }
+  if (p->MT == 1) return launch_pass_t<false, 1>(c, a);
+  return launch_pass_t<false, 2>(c, a);
+}
+
+int launch_system(Ctx& c, int slot) {
+  dba_plan* p = c.p;
+  if (p->NL > 0) {
+    AsmArgs a;
+    a.calib = p->calib;
+    a.nve = p->nve;
+    a.status = c.at<int>(p->L.flags);
+    a.csr_off = c.at<int>(p->L.csr_off);
+    a.slot_edge = c.at<int>(p->L.slot_edge);
+    a.frame_seg = c.at<int>(p->L.frame_seg);
+    a.adj = c.at<double>(p->L.adj);
+    a.part_edge = c.at<double>(p->L.part_edge);
+    a.part_M = c.at<double>(p->L.part_M);
+    a.part_w = c.at<double>(p->L.part_w);
+    a.part_frame = c.at<double>(p->L.part_frame);
+    a.seg_off_edge = c.at<long long>(p->L.seg_off_edge);
+    a.seg_off_M = c.at<long long>(p->L.seg_off_M);
+    a.seg_off_w = c.at<long long>(p->L.seg_off_w);
+    a.Fbuf = c.at<double>(p->L.Fbuf);
+    a.off_F = c.at<long long>(p->L.off_F);
+    a.off_f = c.at<long long>(p->L.off_f);
+    a.bad_edge = c.at<int>(p->L.flags) + 1;
+    assemble_kernel<<<p->NL, 256, 0, c.st>>>(a);
+    DBA_CUDA(cudaGetLastError());
+  }
+  if (p->n_units > 0) {
+    GatherArgs g;
+    g.n_units = p->n_units;
+    g.status = c.at<int>(p->L.flags);
+    g.units = c.at<GatherUnit>(p->L.units);
+    g.contrib = c.at<Contrib>(p->L.contrib);
+    g.Fbuf = c.at<double>(p->L.Fbuf);
+    g.sys = c.at<double>(p->L.sys[slot]);
+    const int threads = 256, warps = threads / 32;
+    gather_kernel<<<(p->n_units + warps - 1) / warps, threads, 0, c.st>>>(g);
+    DBA_CUDA(cudaGetLastError());
+  }
+  FinalArgs f;
+  f.n = p->nseg;
+  f.status = c.at<int>(p->L.flags);
+  f.part_frame = c.at<double>(p->L.part_frame);
+  f.energy_out = c.at<double>(p->L.sys[slot]) + p->energy_off;
+  finalize_kernel<<<1, 256, 0, c.st>>>(f);
+  DBA_CUDA(cudaGetLastError());
+  if (c.comm && p->nranks > 1) {
+    if (!nccl().ok) return DBA_ENCCL;
+    double* s = c.at<double>(p->L.sys[slot]);
+    if (nccl().AllReduce(s, s, (size_t)p->sys_len, ncclDouble, ncclSum, c.comm, c.st) != ncclSuccess)
+      return DBA_ENCCL;
+    int* bad = c.at<int>(p->L.flags) + 1;
+    if (nccl().AllReduce(bad, bad, 1, ncclInt32, ncclMin, c.comm, c.st) != ncclSuccess) return DBA_ENCCL;
+  }
+  return DBA_OK;
+}
+
+int launch_solve(Ctx& c, int slot, double lam) {
+  dba_plan* p = c.p;
+  if (p->n_red == 0) return DBA_OK;
+  SolveArgs a;
+  a.nb = p->nb;
+  a.BW = p->BW;
+  a.calib = p->calib;
+  a.lambda = lam;
+  a.status = c.at<int>(p->L.flags);
+  const double* s = c.at<double>(p->L.sys[slot]);
+  a.band = s;
+  a.theta = s + p->theta_off;
+  a.thth = s + p->thth_off;
+  a.y = s + p->y_off;
+  a.Lband = c.at<double>(p->L.Lband);
+  a.delta = c.at<double>(p->L.delta);
+  a.cond = &c.at<Readback>(p->L.flags)->cond;
+  DBA_CUDA(cudaFuncSetAttribute(solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)p->solve_smem));
+  solve_kernel<<<1, kSolveThreads, p->solve_smem, c.st>>>(a);
+  return cuda_status(cudaGetLastError());
+}
+
+int reset_flags(Ctx& c) {
+  Readback h{};
+  h.status[0] = 0;
+  h.status[1] = INT_MAX;
+  h.cond = 0.0;
+  *c.p->rb = h;
+  DBA_CUDA(cudaMemcpyAsync(c.at<Readback>(c.p->L.flags), c.p->rb, sizeof(Readback),
+                           cudaMemcpyHostToDevice, c.st));
+  return DBA_OK;
+}
+
+int read_flags(Ctx& c, int slot, Readback& out) {
+  dba_plan* p = c.p;
+  DBA_CUDA(cudaMemcpyAsync(p->rb, c.at<Readback>(p->L.flags), sizeof(Readback), cudaMemcpyDeviceToHost,
+                           c.st));
+  DBA_CUDA(cudaMemcpyAsync(&p->rb->energy, c.at<double>(p->L.sys[slot]) + p->energy_off, sizeof(double),
+                           cudaMemcpyDeviceToHost, c.st));
+  DBA_CUDA(cudaStreamSynchronize(c.st));
+  out = *p->rb;
+  return DBA_OK;
+}
+
+// copy inputs into state slot 0 and linearise there (the first pass)
+int initial_pass(Ctx& c) {
+  dba_plan* p = c.p;
+  DBA_CUDA(cudaMemcpyAsync(c.at<double>(p->L.poses[0]), c.b->poses_in, sizeof(double) * 7 * p->N,
+                           cudaMemcpyDeviceToDevice, c.st));
+  DBA_CUDA(cudaMemcpyAsync(c.at<double>(p->L.intr[0]), c.b->intr_in, sizeof(double) * 4,
+                           cudaMemcpyDeviceToDevice, c.st));
+  const size_t fbytes = sizeof(float) * (size_t)p->P;
+  if (p->NL > 0) {
+    DBA_CUDA(cudaMemcpyAsync(c.at<float>(p->L.disps[0]) + (size_t)p->f0 * p->P,
+                             c.b->disps_in + (size_t)p->f0 * p->P, fbytes * p->NL, cudaMemcpyDeviceToDevice,
+                             c.st));
+  }
+  int s = reset_flags(c);
+  if (s) return s;
+  if ((s = launch_prep(c, 0, 0, true))) return s;
+  if ((s = launch_pass(c, 0, 0, false, true))) return s;
+  return launch_system(c, 0);
+}
+
+int gauge_sum(Ctx& c, const float* d, double* out) {
+  dba_plan* p = c.p;
+  const int g = p->gauge_frame;
+  const int frame = (g >= p->f0 && g < p->f1) ? g : -1;
+  logsum_kernel<<<1, 256, 0, c.st>>>(d, frame, p->P, out);
+  DBA_CUDA(cudaGetLastError());
+  if (c.comm && p->nranks > 1 && nccl().ok)
+    if (nccl().AllReduce(out, out, 1, ncclDouble, ncclSum, c.comm, c.st) != ncclSuccess) return DBA_ENCCL;
+  return DBA_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int dba_solve(dba_plan* p, const dba_options* o, const dba_buffers* b, dba_report* rep) {
+  int s = check_args(p, o, b);
+  if (s) return s;
+  if (!rep || !b->poses_out || !b->disps_out || !b->intr_out) return DBA_EINVAL;
+  if (p->nranks > 1 && !b->nccl_comm) return DBA_EINVAL;
+  std::memset(rep, 0, sizeof(*rep));
+  rep->bad_edge = -1;
+  rep->scale = 1.0;
+  Ctx c{p, o, b, reinterpret_cast<cudaStream_t>(b->stream), reinterpret_cast<unsigned char*>(b->workspace),
+        reinterpret_cast<ncclComm_t>(b->nccl_comm)};
+  if ((s = prepare(c))) return rep->status = s;
+  double* gsum = c.at<double>(p->L.gauge);
+  if (p->gauge_on)
+    if ((s = gauge_sum(c, b->disps_in, gsum))) return rep->status = s;
+  if ((s = initial_pass(c))) return rep->status = s;
+  Readback rb;
+  if ((s = read_flags(c, 0, rb))) return rep->status = s;
+  if (rb.status[1] != INT_MAX || !std::isfinite(rb.energy)) {
+    rep->bad_edge = rb.status[1] != INT_MAX ? rb.status[1] : -1;
+    return rep->status = DBA_ENONFINITE;
+  }
+  double Ec = rb.energy;
+  rep->initial_energy = Ec;
+  double lam = o->lambda0;
+  int cur = 0, it = 0;
+  while (it < o->iters) {
+    const int nxt = 1 - cur;
+    if ((s = reset_flags(c))) return rep->status = s;
+    if ((s = launch_solve(c, cur, lam))) return rep->status = s;
+    if ((s = launch_prep(c, cur, nxt, false))) return rep->status = s;
+    if ((s = launch_pass(c, cur, nxt, true, true))) return rep->status = s;
+    if ((s = launch_system(c, nxt))) return rep->status = s;
+    if ((s = read_flags(c, nxt, rb))) return rep->status = s;
+    if (rb.status[0] != 0) {  // factorisation failed: more damping
+      lam *= 10.0;
+      if (lam > o->lambda_max) return rep->status = DBA_ESOLVER;
+      continue;
+    }
+    rep->trials++;
+    if (p->calib) {
+      rep->calib_condition = rb.cond;
+      if (o->calib_cond_max > 0 && rb.cond > o->calib_cond_max) return rep->status = DBA_ECALIB;
+    }
+    if (rb.status[1] != INT_MAX || !std::isfinite(rb.energy)) {
+      rep->bad_edge = rb.status[1] != INT_MAX ? rb.status[1] : -1;
+      return rep->status = DBA_ENONFINITE;
+    }
+    if (rb.energy <= Ec) {
+      cur = nxt;
+      Ec = rb.energy;
+      lam = std::max(lam / 10.0, o->lambda_min);
+      if (rep->trace_len < DBA_TRACE_MAX) rep->energy_trace[rep->trace_len++] = Ec;
+      ++it;
+    } else {
+      lam *= 10.0;
+      if (lam > o->lambda_max) {
+        rep->converged = 1;
+        break;
+      }
+    }
+  }
+  rep->iterations = it;
+  rep->final_energy = Ec;
+  rep->lambda_final = lam;
+  // outputs
+  DBA_CUDA(cudaMemcpyAsync(b->poses_out, c.at<double>(p->L.poses[cur]), sizeof(double) * 7 * p->N,
+                           cudaMemcpyDeviceToDevice, c.st));
+  DBA_CUDA(cudaMemcpyAsync(b->intr_out, c.at<double>(p->L.intr[cur]), sizeof(double) * 4,
+                           cudaMemcpyDeviceToDevice, c.st));
+  if (p->NL > 0)
+    DBA_CUDA(cudaMemcpyAsync(b->disps_out + (size_t)p->f0 * p->P, c.at<float>(p->L.disps[cur]) + (size_t)p->f0 * p->P,
+                             sizeof(float) * (size_t)p->P * p->NL, cudaMemcpyDeviceToDevice, c.st));
+  if (p->gauge_on) {
+    if ((s = gauge_sum(c, b->disps_out, gsum + 1))) return rep->status = s;
+    GaugeArgs g;
+    g.N = p->N;
+    g.P = p->P;
+    g.g = p->gauge_frame;
+    g.f0 = p->f0;
+    g.f1 = p->f1;
+    g.d_min = o->d_min;
+    g.ref_sum = gsum;
+    g.cur_sum = gsum + 1;
+    g.scale_out = gsum + 2;
+    g.d = b->disps_out;
+    g.poses = b->poses_out;
+    const long long n = std::max<long long>((long long)p->NL * p->P, p->N);
+    gauge_apply_kernel<<<(unsigned)((n + 255) / 256), 256, 0, c.st>>>(g);
+    DBA_CUDA(cudaGetLastError());
+    DBA_CUDA(cudaMemcpyAsync(&rep->scale, gsum + 2, sizeof(double), cudaMemcpyDeviceToHost, c.st));
+  }
+  DBA_CUDA(cudaStreamSynchronize(c.st));
+  rep->status = DBA_OK;
+  return DBA_OK;
+}
+
+int dba_energy(dba_plan* p, const dba_options* o, const dba_buffers* b, double* energy) {
+  int s = check_args(p, o, b);
+  if (s) return s;
+  if (!energy) return DBA_EINVAL;
+  Ctx c{p, o, b, reinterpret_cast<cudaStream_t>(b->stream), reinterpret_cast<unsigned char*>(b->workspace),
+        reinterpret_cast<ncclComm_t>(b->nccl_comm)};
+  if ((s = prepare(c))) return s;
+  if ((s = initial_pass(c))) return s;
+  Readback rb;
+  if ((s = read_flags(c, 0, rb))) return s;
+  *energy = rb.energy;
+  return DBA_OK;
+}
+
+int dba_build_system(dba_plan* p, const dba_options* o, const dba_buffers* b, double* S, double* y,
+                     double* energy) {
+  int s = check_args(p, o, b);
+  if (s) return s;
+  if (!S || !y || !energy) return DBA_EINVAL;
+  Ctx c{p, o, b, reinterpret_cast<cudaStream_t>(b->stream), reinterpret_cast<unsigned char*>(b->workspace),
+        reinterpret_cast<ncclComm_t>(b->nccl_comm)};
+  if ((s = prepare(c))) return s;
+  if ((s = initial_pass(c))) return s;
+  std::vector<double> sys(p->sys_len);
+  DBA_CUDA(cudaMemcpyAsync(sys.data(), c.at<double>(p->L.sys[0]), sizeof(double) * p->sys_len,
+                           cudaMemcpyDeviceToHost, c.st));
+  DBA_CUDA(cudaStreamSynchronize(c.st));
+  const int n = p->n_red, W1 = p->BW + 1;
+  std::fill(S, S + (size_t)n * n, 0.0);
+  for (int a = 0; a < p->nb; ++a)
+    for (int pos = 0; pos < W1; ++pos) {
+      const int cb = a - p->BW + pos;
+      if (cb < 0) continue;
+      const double* blk = sys.data() + ((size_t)a * W1 + pos) * 36;
+      for (int r = 0; r < 6; ++r)
+        for (int q = 0; q < 6; ++q) {
+          S[(size_t)(6 * a + r) * n + 6 * cb + q] = blk[6 * r + q];
+          S[(size_t)(6 * cb + q) * n + 6 * a + r] = blk[6 * r + q];
+        }
+    }
+  if (p->calib) {
+    const int t0 = 6 * p->nb;
+    for (int cb = 0; cb < p->nb; ++cb)
+      for (int t = 0; t < 4; ++t)
+        for (int q = 0; q < 6; ++q) {
+          const double v = sys[p->theta_off + (size_t)cb * 24 + 6 * t + q];
+          S[(size_t)(t0 + t) * n + 6 * cb + q] = v;
+          S[(size_t)(6 * cb + q) * n + t0 + t] = v;
+        }
+    for (int t = 0; t < 4; ++t)
+      for (int u = 0; u < 4; ++u) S[(size_t)(t0 + t) * n + t0 + u] = sys[p->thth_off + 4 * t + u];
+  }
+  for (int x = 0; x < n; ++x) y[x] = sys[p->y_off + x];
+  *energy = sys[p->energy_off];
+  return DBA_OK;
+}
+
+int dba_nccl_unique_id(uint8_t id_out[128]) {
+  if (!nccl().ok) return DBA_ENCCL;
+  ncclUniqueId id;
+  if (nccl().GetUniqueId(&id) != ncclSuccess) return DBA_ENCCL;
+  static_assert(sizeof(ncclUniqueId) == 128, "nccl id size");
+  std::memcpy(id_out, &id, 128);
+  return DBA_OK;
+}
+
+int dba_nccl_comm_init(int32_t nranks, const uint8_t id[128], int32_t rank, void** comm_out) {
+  if (!id || !comm_out) return DBA_EINVAL;
+  if (!nccl().ok) return DBA_ENCCL;
+  ncclUniqueId uid;
+  std::memcpy(&uid, id, 128);
+  ncclComm_t comm;
+  if (nccl().CommInitRank(&comm, nranks, uid, rank) != ncclSuccess) return DBA_ENCCL;
+  *comm_out = comm;
+  return DBA_OK;
+}
+
+int dba_nccl_comm_destroy(void* comm) {
+  if (!comm) return DBA_EINVAL;
+  if (!nccl().ok) return DBA_ENCCL;
+  return nccl().CommDestroy(reinterpret_cast<ncclComm_t>(comm)) == ncclSuccess ? DBA_OK : DBA_ENCCL;
+}
+
+}  // extern "C"

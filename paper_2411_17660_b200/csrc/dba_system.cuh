@@ -1,0 +1,377 @@
+// Small per-pose / per-edge / per-frame kernels around the fused pass:
+//   prep_kernel      K4: clamped tangent step -> retraction exp(xi) o G (float64),
+//                    per-edge constants for the next pass (both states)
+//   assemble_kernel  per source frame: split partials -> frame factor F_i over the
+//                    local variables [i, j_e..., theta] (float64):
+//                    F_i = sum_e B_e - T M T^T,  f_i = sum_e g_e - T w
+//   gather_kernel    deterministic scatter-free assembly of the banded reduced
+//                    system from the frame factors (host-built contribution lists)
+//   finalize_kernel  fixed-order energy reduction
+//   gauge kernels    A5 scale gauge at the end of a solve
+#pragma once
+
+#include "dba_common.cuh"
+
+namespace dba {
+
+// ---------------------------------------------------------------- prep (K4)
+
+struct PrepArgs {
+  int N, EL, init, calib, theta_off;
+  double tmax;
+  const int* status;
+  const int* ridx;
+  const int* slot_i;
+  const int* slot_j;
+  const double* poses_c;
+  double* poses_n;
+  const double* intr_c;
+  double* intr_n;
+  const double* delta;
+  double* xi_out;  // (N,6) clamped steps actually applied
+  EdgeLin* lin;
+  EdgeBack* back;
+  double* adj;  // (EL,36) Ad(G_ij) at x_n
+};
+
+__device__ inline void clamped_xi(const PrepArgs& A, int k, double xi[6]) {
+  for (int c = 0; c < 6; ++c) xi[c] = 0.0;
+  if (A.init) return;
+  const int r = A.ridx[k];
+  if (r < 0) return;
+  double n2 = 0.0;
+  for (int c = 0; c < 6; ++c) {
+    xi[c] = A.delta[6 * r + c];
+    n2 += xi[c] * xi[c];
+  }
+  const double n = sqrt(n2);
+  if (n > A.tmax) {
+    const double s = A.tmax / n;
+    for (int c = 0; c < 6; ++c) xi[c] *= s;
+  }
+}
+
+__device__ inline Pose64 stepped_pose(const PrepArgs& A, int k, const double xi[6]) {
+  const Pose64 pc = load_pose(A.poses_c + 7 * k);
+  if (A.init || A.ridx[k] < 0) return pc;
+  return compose(se3_exp(xi), pc);
+}
+
+__global__ void prep_kernel(const PrepArgs A) {
+  if (A.status != nullptr && A.status[0] != 0) return;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < A.N) {
+    double xi[6];
+    clamped_xi(A, t, xi);
+    for (int c = 0; c < 6; ++c) A.xi_out[6 * t + c] = xi[c];
+    if (A.init || A.ridx[t] < 0) {
+      for (int c = 0; c < 7; ++c) A.poses_n[7 * t + c] = A.poses_c[7 * t + c];
+    } else {
+      store_pose(stepped_pose(A, t, xi), A.poses_n + 7 * t);
+    }
+  } else if (t < A.N + A.EL) {
+    const int s = t - A.N;
+    const int i = A.slot_i[s], j = A.slot_j[s];
+    double xi_i[6], xi_j[6];
+    clamped_xi(A, i, xi_i);
+    clamped_xi(A, j, xi_j);
+    const Pose64 ci = load_pose(A.poses_c + 7 * i), cj = load_pose(A.poses_c + 7 * j);
+    const Pose64 gc = compose(cj, inverse(ci));
+    const Pose64 gn = compose(stepped_pose(A, j, xi_j), inverse(stepped_pose(A, i, xi_i)));
+    double Rn[9], Rc[9], Ac[36], An[36];
+    quat_to_rot(gn.q, Rn);
+    quat_to_rot(gc.q, Rc);
+    adjoint(Rn, gn.t, An);
+    adjoint(Rc, gc.t, Ac);
+    EdgeLin el;
+    EdgeBack eb;
+    for (int c = 0; c < 9; ++c) {
+      el.R[c] = (float)Rn[c];
+      eb.R[c] = (float)Rc[c];
+    }
+    for (int c = 0; c < 3; ++c) {
+      el.t[c] = (float)gn.t[c];
+      eb.t[c] = (float)gc.t[c];
+    }
+    for (int r = 0; r < 6; ++r) {
+      double s2 = xi_j[r];
+      for (int c = 0; c < 6; ++c) s2 -= Ac[6 * r + c] * xi_i[c];
+      eb.dlt[r] = (float)s2;
+    }
+    eb.pad[0] = eb.pad[1] = 0.f;
+    A.lin[s] = el;
+    A.back[s] = eb;
+    for (int c = 0; c < 36; ++c) A.adj[36 * (size_t)s + c] = An[c];
+  } else if (t == A.N + A.EL) {
+    for (int c = 0; c < 4; ++c) {
+      const double d = (A.calib && !A.init) ? A.delta[A.theta_off + c] : 0.0;
+      A.intr_n[c] = A.intr_c[c] + d;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- assemble
+
+struct AsmArgs {
+  int calib, nve;
+  const int* status;
+  const int* csr_off;
+  const int* slot_edge;
+  const int* frame_seg;  // local frame -> segment range
+  const double* adj;
+  const double* part_edge;
+  const double* part_M;
+  const double* part_w;
+  const double* part_frame;
+  const long long* seg_off_edge;
+  const long long* seg_off_M;
+  const long long* seg_off_w;
+  double* Fbuf;
+  const long long* off_F;
+  const long long* off_f;
+  int* bad_edge;
+};
+
+__device__ __forceinline__ int tri6(int r, int c) {
+  if (r > c) {
+    const int t = r;
+    r = c;
+    c = t;
+  }
+  return r * 6 - r * (r - 1) / 2 + (c - r);
+}
+__device__ __forceinline__ int tri4(int r, int c) {
+  if (r > c) {
+    const int t = r;
+    r = c;
+    c = t;
+  }
+  return r * 4 - r * (r - 1) / 2 + (c - r);
+}
+
+__global__ void __launch_bounds__(256) assemble_kernel(const AsmArgs A) {
+  if (A.status != nullptr && A.status[0] != 0) return;
+  __shared__ double Ad[kMaxOutDegree * 36];
+  __shared__ double hs[kMaxOutDegree * (kEdgeVals + kCalibVals)];
+  __shared__ double ws[6 * kMaxOutDegree + 4];
+  __shared__ double fs[kFrameVals];
+  __shared__ double Nm[6 * (6 * kMaxOutDegree + 4)];
+  const int fl = blockIdx.x, tid = threadIdx.x;
+  const int s0 = A.csr_off[fl], k = A.csr_off[fl + 1] - s0;
+  if (k == 0) return;
+  const int nve = A.nve;
+  const int mu = 6 * k + (A.calib ? 4 : 0), m = mu + 6;
+  double* F = A.Fbuf + A.off_F[fl];
+  double* fv = A.Fbuf + A.off_f[fl];
+  const int sg0 = A.frame_seg[fl], sg1 = A.frame_seg[fl + 1];
+
+  for (int x = tid; x < k * 36; x += blockDim.x) Ad[x] = A.adj[36 * (size_t)s0 + x];
+  for (int x = tid; x < k * nve; x += blockDim.x) {
+    double s = 0.0;
+    for (int sg = sg0; sg < sg1; ++sg) s += A.part_edge[A.seg_off_edge[sg] + x];
+    hs[x] = s;
+  }
+  for (int x = tid; x < mu; x += blockDim.x) {
+    double s = 0.0;
+    for (int sg = sg0; sg < sg1; ++sg) s += A.part_w[A.seg_off_w[sg] + x];
+    ws[x] = s;
+  }
+  if (tid < kFrameVals) {
+    double s = 0.0;
+    for (int sg = sg0; sg < sg1; ++sg) s += A.part_frame[(long long)sg * kFrameVals + tid];
+    fs[tid] = s;
+  }
+  for (int x = tid; x < mu * mu; x += blockDim.x) {
+    double s = 0.0;
+    for (int sg = sg0; sg < sg1; ++sg) s += A.part_M[A.seg_off_M[sg] + x];
+    const int r = x / mu, c = x % mu;
+    F[(long long)(6 + r) * m + 6 + c] = -s;
+  }
+  __syncthreads();
+  if (tid < k) {
+    bool ok = true;
+    for (int x = 0; x < nve; ++x) ok = ok && isfinite(hs[tid * nve + x]);
+    if (!ok) atomicMin(A.bad_edge, A.slot_edge[s0 + tid]);
+  }
+  // N = sum_e Ad_e^T M[e, :]   (6 x mu); F currently holds -M in the u x u block
+  for (int x = tid; x < 6 * mu; x += blockDim.x) {
+    const int r = x / mu, c = x % mu;
+    double s = 0.0;
+    for (int e = 0; e < k; ++e)
+      for (int q = 0; q < 6; ++q) s -= Ad[36 * e + 6 * q + r] * F[(long long)(6 + 6 * e + q) * m + 6 + c];
+    Nm[x] = s;
+  }
+  __syncthreads();
+  const int th0 = 6 * k;  // theta offset in u-space
+  for (int x = tid; x < m * m; x += blockDim.x) {
+    const int r = x / m, c = x % m;
+    if (r >= 6 && c >= 6) {
+      const int ru = r - 6, cu = c - 6;
+      double b = 0.0;
+      const bool rt = A.calib && ru >= th0, ct = A.calib && cu >= th0;
+      if (!rt && !ct) {
+        if (ru / 6 == cu / 6) b = hs[(ru / 6) * nve + tri6(ru % 6, cu % 6)];
+      } else if (rt && !ct) {
+        b = hs[(cu / 6) * nve + 32 + 6 * (ru - th0) + cu % 6];
+      } else if (!rt && ct) {
+        b = hs[(ru / 6) * nve + 32 + 6 * (cu - th0) + ru % 6];
+      } else {
+        b = fs[1 + tri4(ru - th0, cu - th0)];
+      }
+      F[x] += b;
+    } else if (r < 6 && c < 6) {
+      double s = 0.0;
+      for (int e = 0; e < k; ++e) {
+        const double* Ae = Ad + 36 * e;
+        const double* He = hs + e * nve;
+        // + Ad_e^T H_e Ad_e   - N_e Ad_e
+        for (int q = 0; q < 6; ++q) {
+          double hq = 0.0;
+          for (int u = 0; u < 6; ++u) hq += Ae[6 * u + r] * He[tri6(u, q)];
+          s += (hq - Nm[r * mu + 6 * e + q]) * Ae[6 * q + c];
+        }
+      }
+      F[x] = s;
+    } else {
+      const int rr = r < 6 ? r : c;       // pose-i row (0..5)
+      const int cu = r < 6 ? c - 6 : r - 6;  // u-space column
+      double b = 0.0;
+      if (A.calib && cu >= th0) {
+        const int t = cu - th0;
+        for (int e = 0; e < k; ++e)
+          for (int q = 0; q < 6; ++q) b -= hs[e * nve + 32 + 6 * t + q] * Ad[36 * e + 6 * q + rr];
+      } else {
+        const int e = cu / 6, cc = cu % 6;
+        for (int q = 0; q < 6; ++q) b -= Ad[36 * e + 6 * q + rr] * hs[e * nve + tri6(q, cc)];
+      }
+      F[x] = Nm[rr * mu + cu] + b;
+    }
+  }
+  for (int x = tid; x < m; x += blockDim.x) {
+    double v;
+    if (x < 6) {
+      v = 0.0;
+      for (int e = 0; e < k; ++e)
+        for (int q = 0; q < 6; ++q) v += Ad[36 * e + 6 * q + x] * (ws[6 * e + q] - hs[e * nve + 21 + q]);
+    } else {
+      const int cu = x - 6;
+      if (A.calib && cu >= th0)
+        v = fs[11 + cu - th0] - ws[cu];
+      else
+        v = hs[(cu / 6) * nve + 21 + cu % 6] - ws[cu];
+    }
+    fv[x] = v;
+  }
+}
+
+// ---------------------------------------------------------------- gather
+
+struct GatherUnit {
+  long long dst;
+  int rows, cols, c0, c1;
+};
+struct Contrib {
+  long long src;
+  int stride, pad;
+};
+
+struct GatherArgs {
+  int n_units;
+  const int* status;
+  const GatherUnit* units;
+  const Contrib* contrib;
+  const double* Fbuf;
+  double* sys;
+};
+
+__global__ void gather_kernel(const GatherArgs A) {
+  if (A.status != nullptr && A.status[0] != 0) return;
+  const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (wid >= A.n_units) return;
+  const GatherUnit u = A.units[wid];
+  const int n = u.rows * u.cols;
+  for (int e = lane; e < n; e += 32) {
+    const int r = e / u.cols, c = e % u.cols;
+    double s = 0.0;
+    for (int q = u.c0; q < u.c1; ++q) {
+      const Contrib cb = A.contrib[q];
+      s += A.Fbuf[cb.src + (long long)r * cb.stride + c];
+    }
+    A.sys[u.dst + e] = s;
+  }
+}
+
+// ---------------------------------------------------------------- finalize
+
+struct FinalArgs {
+  int n;  // number of frame-partial rows (segments)
+  const int* status;
+  const double* part_frame;
+  double* energy_out;
+};
+
+__global__ void __launch_bounds__(256) finalize_kernel(const FinalArgs A) {
+  if (A.status != nullptr && A.status[0] != 0) return;
+  __shared__ double sh[256];
+  double s = 0.0;
+  for (int x = threadIdx.x; x < A.n; x += 256) s += A.part_frame[(long long)x * kFrameVals];
+  sh[threadIdx.x] = s;
+  __syncthreads();
+  for (int off = 128; off >= 1; off >>= 1) {
+    if ((int)threadIdx.x < off) sh[threadIdx.x] += sh[threadIdx.x + off];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) A.energy_out[0] = sh[0];
+}
+
+// ---------------------------------------------------------------- gauge (A5)
+
+// sum of log d over one frame (fixed-order tree); out[0] = sum (0 if frame < 0)
+__global__ void __launch_bounds__(256) logsum_kernel(const float* d, int frame, int P, double* out) {
+  __shared__ double sh[256];
+  double s = 0.0;
+  if (frame >= 0)
+    for (int x = threadIdx.x; x < P; x += 256) s += log((double)d[(size_t)frame * P + x]);
+  sh[threadIdx.x] = s;
+  __syncthreads();
+  for (int off = 128; off >= 1; off >>= 1) {
+    if ((int)threadIdx.x < off) sh[threadIdx.x] += sh[threadIdx.x + off];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[0] = sh[0];
+}
+
+struct GaugeArgs {
+  int N, P, g, f0, f1;
+  double d_min;
+  const double* ref_sum;  // sum log d_g at the input state
+  const double* cur_sum;  // sum log d_g at the final state
+  double* scale_out;
+  float* d;
+  double* poses;
+};
+
+// d <- max(s d, d_min) on this rank's frames; every pose moved by the similarity
+// about camera g that keeps G_g:  t_k <- (t_k - c_k)/s + c_k,  c_k = R_k R_g^T t_g
+__global__ void gauge_apply_kernel(const GaugeArgs A) {
+  const double s = exp((A.ref_sum[0] - A.cur_sum[0]) / (double)A.P);
+  const long long n_d = (long long)(A.f1 - A.f0) * A.P;
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t == 0) A.scale_out[0] = s;
+  if (t < n_d) {
+    float* dp = A.d + (long long)A.f0 * A.P + t;
+    *dp = fmaxf(*dp * (float)s, (float)A.d_min);
+  }
+  if (t < A.N && t != A.g) {
+    const Pose64 pg = load_pose(A.poses + 7 * A.g);
+    const Pose64 pk = load_pose(A.poses + 7 * t);
+    double Rg[9], Rk[9], w[3], c[3];
+    quat_to_rot(pg.q, Rg);
+    quat_to_rot(pk.q, Rk);
+    for (int r = 0; r < 3; ++r) w[r] = Rg[r] * pg.t[0] + Rg[3 + r] * pg.t[1] + Rg[6 + r] * pg.t[2];
+    for (int r = 0; r < 3; ++r) c[r] = Rk[3 * r] * w[0] + Rk[3 * r + 1] * w[1] + Rk[3 * r + 2] * w[2];
+    for (int r = 0; r < 3; ++r) A.poses[7 * t + 4 + r] = (pk.t[r] - c[r]) / s + c[r];
+  }
+}
+
+}  // namespace dba

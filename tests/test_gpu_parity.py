@@ -1,0 +1,121 @@
+"""GPU parity: the sm_100a path through the C-ABI vs the float64 CPU oracle.
+
+Tolerances (SURVEY §8d / north star): relative 1e-4 on every disparity and pose
+translation after each GN iteration; rotation angle within 1e-4 deg-equivalent;
+reduced system S, y relative 1e-4 (Frobenius, fp32 per-pixel math with fp64
+cross-tile accumulation); energies relative 1e-4.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from oracle import dba as O
+from tests.helpers import oracle_problem, oracle_state, pose_errors, small_workload
+
+pytestmark = pytest.mark.gpu
+
+REL_TOL = 1e-4
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("GPU tests require a CUDA device")
+    return torch
+
+
+def _solver(wl, calib=False, prior=False, fixed=None, scale_gauge=None):
+    from paper_2411_17660_b200 import dba
+    return dba.DBASolver(wl.ii, wl.jj, len(wl.frames), wl.flow.shape[1], wl.flow.shape[2],
+                         wl.fixed if fixed is None else fixed, optimize_intrinsics=calib,
+                         use_prior=prior, scale_gauge=scale_gauge)
+
+
+def _rel(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+@pytest.mark.parametrize("cfg", ["C1", "C2"])
+def test_system_parity(torch_cuda, cfg):
+    wl = small_workload(cfg, keyframes=8 if cfg == "C2" else None)
+    s = _solver(wl)
+    S, y, e = s.build_system(wl.poses0, wl.disps0, wl.intr0, wl.flow)
+    st = oracle_state(wl, disps=wl.disps0)
+    sysm = O.linearize(st, oracle_problem(wl), O.Options())
+    Sr, yr, _ = O.reduced(sysm, oracle_problem(wl), O.Options())
+    assert S.shape == Sr.shape
+    assert _rel(S, Sr) < REL_TOL, _rel(S, Sr)
+    assert _rel(y, yr) < REL_TOL, _rel(y, yr)
+    assert abs(e - sysm.energy) / sysm.energy < REL_TOL
+
+
+def test_system_parity_calib_prior(torch_cuda):
+    wl = small_workload("C5", keyframes=6, radius=2)
+    s = _solver(wl, calib=True)
+    S, y, e = s.build_system(wl.poses0, wl.disps0, wl.intr0, wl.flow)
+    opts = O.Options(optimize_intrinsics=True)
+    sysm = O.linearize(oracle_state(wl), oracle_problem(wl), opts)
+    Sr, yr, _ = O.reduced(sysm, oracle_problem(wl), opts)
+    assert _rel(S, Sr) < REL_TOL, _rel(S, Sr)
+    assert _rel(y, yr) < REL_TOL, _rel(y, yr)
+    wl4 = small_workload("C4", keyframes=6)
+    s4 = _solver(wl4, prior=True)
+    S4, y4, e4 = s4.build_system(wl4.poses0, wl4.disps0, wl4.intr0, wl4.flow, wl4.prior,
+                                 wl4.prior_mask)
+    opts4 = O.Options()
+    sys4 = O.linearize(oracle_state(wl4), oracle_problem(wl4, prior=True), opts4)
+    Sr4, yr4, _ = O.reduced(sys4, oracle_problem(wl4, prior=True), opts4)
+    assert _rel(S4, Sr4) < REL_TOL
+    assert _rel(y4, yr4) < REL_TOL
+    assert abs(e4 - sys4.energy) / sys4.energy < REL_TOL
+
+
+@pytest.mark.parametrize("iters", [1, 2, 3])
+def test_solve_parity_per_iteration(torch_cuda, iters):
+    wl = small_workload("C1")
+    s = _solver(wl)
+    Po, Do, Ko, rep = s.solve(wl.poses0, wl.disps0, wl.intr0, wl.flow, iters=iters)
+    ref, rrep = O.solve(oracle_state(wl), oracle_problem(wl), O.Options(iters=iters))
+    assert rep.iterations_run == rrep.iterations
+    te, ae = pose_errors(Po.cpu().numpy(), ref.poses)
+    assert te < REL_TOL, te
+    assert ae < 1e-3, ae
+    d = Do.cpu().numpy().astype(np.float64)
+    rel = np.abs(d - ref.disps) / ref.disps
+    assert rel.max() < REL_TOL, (rel.max(), np.quantile(rel, 0.999))
+    assert abs(rep.final_energy - rrep.final_energy) <= REL_TOL * rrep.initial_energy
+
+
+def test_energy_parity_and_truth(torch_cuda):
+    wl = small_workload("C1")
+    s = _solver(wl)
+    e = s.energy(wl.poses0, wl.disps0, wl.intr0, wl.flow)
+    eo = O.energy(oracle_state(wl), oracle_problem(wl))
+    assert abs(e - eo) / eo < REL_TOL
+    et = s.energy(wl.true_poses, wl.true_disps.astype(np.float32), wl.true_intr, wl.flow)
+    assert et < 1e-6 * eo
+
+
+def test_fixed_pose_bitwise_and_determinism(torch_cuda):
+    wl = small_workload("C1")
+    s = _solver(wl)
+    a = s.solve(wl.poses0, wl.disps0, wl.intr0, wl.flow, iters=2)
+    b = s.solve(wl.poses0, wl.disps0, wl.intr0, wl.flow, iters=2)
+    assert np.array_equal(a[0].cpu().numpy(), b[0].cpu().numpy())
+    assert np.array_equal(a[1].cpu().numpy(), b[1].cpu().numpy())
+    assert np.array_equal(a[0].cpu().numpy()[0], wl.poses0[0])
+
+
+def test_nonfinite_names_edge(torch_cuda):
+    from paper_2411_17660_b200.errors import NumericalError
+    wl = small_workload("C1")
+    flow = wl.flow.copy()
+    flow[5, 3, 4, 0] = np.nan
+    flow[5, 3, 4, 2] = 1.0
+    s = _solver(wl)
+    with pytest.raises(NumericalError) as ei:
+        s.solve(wl.poses0, wl.disps0, wl.intr0, flow, iters=1)
+    assert ei.value.edge == 5
