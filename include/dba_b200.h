@@ -165,6 +165,12 @@ int dba_energy(dba_plan* plan, const dba_options* opt, const dba_buffers* buf,
 int dba_build_system(dba_plan* plan, const dba_options* opt, const dba_buffers* buf,
                      double* S_host, double* y_host, double* energy);
 
+/* Test hook: linearise at the input state, solve (S + lambda I) once, run one
+ * trial pass, and return the step (n_reduced,), the trial poses (N,7), the
+ * trial disparities (N,H,W) and intrinsics (4,) (all HOST) and the trial energy. */
+int dba_debug_trial(dba_plan* plan, const dba_options* opt, const dba_buffers* buf, double lambda,
+                    double* delta, double* poses_n, float* disps_n, double* intr_n, double* energy_n);
+
 /* NCCL bootstrap helpers (the library links NCCL; ids travel as 128 bytes). */
 int dba_nccl_unique_id(uint8_t id_out[128]);
 int dba_nccl_comm_init(int32_t nranks, const uint8_t id[128], int32_t rank, void** comm_out);

@@ -17,10 +17,21 @@ CUDA path:
                        A non-positive Cholesky pivot counts as a reject; if that
                        happens beyond lam_max -> SolverFailure.
   A5  mono gauge       pose(s) in ``fixed`` never move; when exactly one pose is
-                       fixed and no disparity prior is used, the scale is pinned
-                       once at the end of the call: s = exp(mean log d_g(input) -
-                       mean log d_g), d <- s*d, and every pose is moved by the
-                       similarity about camera g that keeps G_g.
+                       fixed and no disparity prior is used ("fix the mean
+                       log-disparity of the first keyframe") every GN
+                       step obeys the linearised, observation-weighted constraint
+                       sum_p C_p dd_g,p / d_g,p = 0 on the gauge frame g (a hard
+                       constraint eliminated with Sherman-Morrison: with c = C/d_g,
+                       h = E C^-1 c = sum_p v_p / d_p, gamma = sum_p C_p / d_p^2,
+                       rho = sum_p g_d,p / d_p the Schur complement gains
+                       + h h^T / gamma, the rhs + h rho / gamma, and the
+                       back-substitution becomes dd_p = r_p / C_p - kappa / d_p with
+                       kappa = (rho - h . dx) / gamma).  Weighting by C keeps
+                       unobserved pixels (C = eta) from absorbing the constraint.
+                       The exact unweighted gauge is applied once at the end of the
+                       call: s = exp(mean log d_g(input) - mean log d_g), d <- s*d,
+                       and every pose moves by the similarity about camera g that
+                       keeps G_g.
   A6  tangent clamp    per pose, ||xi_k||_2 <= 1, applied before back-substitution
                        (SPEC.md:381)
   A7  prior mask       explicit (N,H,W) mask input; C += alpha*m,
@@ -213,7 +224,9 @@ class System:
 
 
 def _frame_terms(state, prob, opts, i, edges, calib, want_hessian):
-    """Per-source-frame accumulation: C, g_d, coupling U (P, m) and the B blocks."""
+    """Per-source-frame accumulation: C, g_d, coupling U (P, m) and the B blocks.
+
+    U's columns are the local variables [i, j_e (CSR order), theta] (v-space)."""
     N = state.poses.shape[0]
     P = state.disps[i].size
     k = len(edges)
@@ -297,6 +310,8 @@ def linearize(state: State, prob: Problem, opts: Options, frames=None,
     edge_energy = np.zeros(E)
     edge_finite = np.ones(E, dtype=bool)
     frame_list = range(N) if frames is None else frames
+    g_frame = gauge_frame(prob, opts)
+    gauge_terms = None
     for i in frame_list:
         edges = [int(x) for x in order[offs[i]:offs[i + 1]]]
         U, C, gd, en, eng_e, fin_e, blocks, grads = _frame_terms(
@@ -320,7 +335,28 @@ def linearize(state: State, prob: Problem, opts: Options, frames=None,
         Uc = U / C[:, None]
         S[np.ix_(idx, idx)] -= U.T @ Uc
         y[idx] -= Uc.T @ gd
-    return System(S, y, energy, edge_energy, edge_finite, Cs, gds, Bm)
+        if i == g_frame:
+            h, gam, rho = _gauge_terms(state, i, U, C, gd)
+            S[np.ix_(idx, idx)] += np.outer(h, h) / gam
+            y[idx] += h * rho / gam
+            gauge_terms = (h, gam, rho)
+    out = System(S, y, energy, edge_energy, edge_finite, Cs, gds, Bm)
+    out.gauge = gauge_terms
+    return out
+
+
+def gauge_frame(prob: Problem, opts: Options):
+    """Index of the gauge frame (first fixed pose) when the mono gauge is on, else -1."""
+    if not use_scale_gauge(prob, opts):
+        return -1
+    return int(np.flatnonzero(prob.fixed)[0])
+
+
+def _gauge_terms(state, i, U, C, gd):
+    """A5 with c = C / d_i:  h = E C^-1 c = U^T (1/d),  gamma = sum C / d^2,
+    rho = sum g_d / d."""
+    inv_d = 1.0 / state.disps[i].reshape(-1)
+    return U.T @ inv_d, float(np.sum(C * inv_d * inv_d)), float(np.sum(gd * inv_d))
 
 
 def energy(state: State, prob: Problem, opts: Options | None = None) -> float:
@@ -392,13 +428,18 @@ def backsub_and_retract(state: State, prob: Problem, opts: Options, dxi_all, dth
     offs, order = csr_by_source(prob.ii, N)
     new = state.copy()
     frame_list = range(N) if frames is None else frames
+    g_frame = gauge_frame(prob, opts)
     for i in frame_list:
         edges = [int(x) for x in order[offs[i]:offs[i + 1]]]
         U, C, gd, *_ = _frame_terms(state, prob, opts, i, edges, calib, False)
         loc = [dxi_all[i]] + [dxi_all[int(prob.jj[e])] for e in edges]
         loc.append(dth if calib else np.zeros(4))
-        vd = U @ np.concatenate(loc)
+        dloc = np.concatenate(loc)
+        vd = U @ dloc
         dd = (gd - vd) / C
+        if i == g_frame and edges:
+            h, gam, rho = _gauge_terms(state, i, U, C, gd)
+            dd = dd - (rho - h @ dloc) / gam / state.disps[i].reshape(-1)
         new.disps[i] = np.maximum(state.disps[i] + dd.reshape(state.disps[i].shape),
                                   opts.d_min)
     for k in range(N):
@@ -548,9 +589,21 @@ def dense_joint_step(state: State, prob: Problem, opts: Options, lam: float):
     keep = list(free_index(prob.fixed, calib)) + list(range(dof, nv))
     keep = np.array(keep)
     Hk = H[np.ix_(keep, keep)]
+    gk = g[keep]
     npose = len(free_index(prob.fixed, calib))
     Hk[np.arange(npose), np.arange(npose)] += lam
-    x = np.linalg.solve(Hk, g[keep])
+    gf = gauge_frame(prob, opts)
+    if gf >= 0:  # A5: linearised gauge constraint as a KKT row
+        a = np.zeros(len(keep))
+        Cg = np.diag(H)[dof + gf * P:dof + (gf + 1) * P]
+        a[npose + gf * P:npose + (gf + 1) * P] = Cg / state.disps[gf].reshape(-1)
+        K = np.zeros((len(keep) + 1, len(keep) + 1))
+        K[:-1, :-1] = Hk
+        K[:-1, -1] = a
+        K[-1, :-1] = a
+        x = np.linalg.solve(K, np.concatenate([gk, [0.0]]))[:-1]
+    else:
+        x = np.linalg.solve(Hk, gk)
     return x[:npose], x[npose:].reshape(N, h, w)
 
 
@@ -565,10 +618,16 @@ def schur_step(state: State, prob: Problem, opts: Options, lam: float):
     calib = opts.optimize_intrinsics
     offs, order = csr_by_source(prob.ii, N)
     dd_all = np.zeros_like(state.disps)
+    g_frame = gauge_frame(prob, opts)
     for i in range(N):
         edges = [int(x) for x in order[offs[i]:offs[i + 1]]]
         U, C, gd, *_ = _frame_terms(state, prob, opts, i, edges, calib, False)
         loc = [dxi[i]] + [dxi[int(prob.jj[e])] for e in edges]
         loc.append(dth if calib else np.zeros(4))
-        dd_all[i] = ((gd - U @ np.concatenate(loc)) / C).reshape(dd_all[i].shape)
+        dloc = np.concatenate(loc)
+        dd = (gd - U @ dloc) / C
+        if i == g_frame and edges:
+            h, gam, rho = _gauge_terms(state, i, U, C, gd)
+            dd = dd - (rho - h @ dloc) / gam / state.disps[i].reshape(-1)
+        dd_all[i] = dd.reshape(dd_all[i].shape)
     return delta, dd_all

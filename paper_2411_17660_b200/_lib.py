@@ -78,7 +78,7 @@ class PlanInfo(ctypes.Structure):
 EXPORTS = (
     "dba_version", "dba_status_string", "dba_partition", "dba_plan_create", "dba_plan_destroy",
     "dba_plan_get_info", "dba_plan_local_edges", "dba_solve", "dba_energy", "dba_build_system",
-    "dba_nccl_unique_id", "dba_nccl_comm_init", "dba_nccl_comm_destroy",
+    "dba_debug_trial", "dba_nccl_unique_id", "dba_nccl_comm_init", "dba_nccl_comm_destroy",
 )
 
 _lib = None
@@ -122,6 +122,9 @@ def load():
     lib.dba_energy.argtypes = [c_vp, P(Options), P(Buffers), P(c_dbl)]
     lib.dba_build_system.restype = c_i32
     lib.dba_build_system.argtypes = [c_vp, P(Options), P(Buffers), P(c_dbl), P(c_dbl), P(c_dbl)]
+    lib.dba_debug_trial.restype = c_i32
+    lib.dba_debug_trial.argtypes = [c_vp, P(Options), P(Buffers), c_dbl, P(c_dbl), P(c_dbl),
+                                    P(ctypes.c_float), P(c_dbl), P(c_dbl)]
     lib.dba_nccl_unique_id.restype = c_i32
     lib.dba_nccl_unique_id.argtypes = [P(ctypes.c_uint8)]
     lib.dba_nccl_comm_init.restype = c_i32

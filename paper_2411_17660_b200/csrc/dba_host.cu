@@ -75,7 +75,7 @@ struct Layout {
   size_t off_F, off_f, units, contrib, meta_end;
   // state
   size_t poses[2], intr[2], disps[2], xi, delta, lin, back, adj;
-  size_t part_edge, part_M, part_w, part_frame, Fbuf, sys[2], Lband, flags, gauge, total;
+  size_t part_edge, part_M, part_w, part_frame, Fbuf, sys[2], gstate[2], Lband, flags, gauge, total;
 };
 
 }  // namespace
@@ -350,7 +350,7 @@ int dba_plan_create(const dba_problem_desc* d, dba_plan** out) {
     seg_off_w[s] = n_pw;
     n_pe += (long long)k * p->nve;
     n_pM += (long long)mu * mu;
-    n_pw += mu;
+    n_pw += 2LL * mu;
   }
   // frame factors
   std::vector<long long> off_F(p->NL), off_f(p->NL);
@@ -503,6 +503,7 @@ int dba_plan_create(const dba_problem_desc* d, dba_plan** out) {
     L.intr[s] = take(sizeof(double) * 4);
     L.disps[s] = take(sizeof(float) * (size_t)N * p->P);
     L.sys[s] = take(sizeof(double) * p->sys_len);
+    L.gstate[s] = take(sizeof(double) * (6 * kMaxOutDegree + 8));
   }
   L.xi = take(sizeof(double) * 6 * N);
   L.delta = take(sizeof(double) * (p->n_red + 4));
@@ -684,6 +685,8 @@ int launch_pass(Ctx& c, int cur, int nxt, bool backsub, bool system) {
   a.d_min = (float)c.o->d_min;
   a.intr_c = c.at<double>(p->L.intr[cur]);
   a.intr_n = c.at<double>(p->L.intr[nxt]);
+  a.gauge_frame = p->gauge_on ? p->gauge_frame : -1;
+  a.gstate_c = c.at<double>(p->L.gstate[cur]);
   a.part_edge = c.at<double>(p->L.part_edge);
   a.part_M = c.at<double>(p->L.part_M);
   a.part_w = c.at<double>(p->L.part_w);
@@ -721,6 +724,9 @@ int launch_system(Ctx& c, int slot) {
     a.off_F = c.at<long long>(p->L.off_F);
     a.off_f = c.at<long long>(p->L.off_f);
     a.bad_edge = c.at<int>(p->L.flags) + 1;
+    a.gauge_frame = p->gauge_on ? p->gauge_frame : -1;
+    a.frame_of = c.at<int>(p->L.frame_of);
+    a.gstate = c.at<double>(p->L.gstate[slot]);
     assemble_kernel<<<p->NL, 256, 0, c.st>>>(a);
     DBA_CUDA(cudaGetLastError());
   }
@@ -984,6 +990,34 @@ int dba_build_system(dba_plan* p, const dba_options* o, const dba_buffers* b, do
   }
   for (int x = 0; x < n; ++x) y[x] = sys[p->y_off + x];
   *energy = sys[p->energy_off];
+  return DBA_OK;
+}
+
+int dba_debug_trial(dba_plan* p, const dba_options* o, const dba_buffers* b, double lambda, double* delta,
+                    double* poses_n, float* disps_n, double* intr_n, double* energy_n) {
+  int s = check_args(p, o, b);
+  if (s) return s;
+  Ctx c{p, o, b, reinterpret_cast<cudaStream_t>(b->stream), reinterpret_cast<unsigned char*>(b->workspace),
+        reinterpret_cast<ncclComm_t>(b->nccl_comm)};
+  if ((s = prepare(c))) return s;
+  if ((s = initial_pass(c))) return s;
+  if ((s = reset_flags(c))) return s;
+  if ((s = launch_solve(c, 0, lambda))) return s;
+  if ((s = launch_prep(c, 0, 1, false))) return s;
+  if ((s = launch_pass(c, 0, 1, true, true))) return s;
+  if ((s = launch_system(c, 1))) return s;
+  Readback rb;
+  if ((s = read_flags(c, 1, rb))) return s;
+  if (rb.status[0]) return DBA_ESOLVER;
+  if (delta && p->n_red > 0)
+    DBA_CUDA(cudaMemcpy(delta, c.at<double>(p->L.delta), sizeof(double) * p->n_red, cudaMemcpyDeviceToHost));
+  if (poses_n)
+    DBA_CUDA(cudaMemcpy(poses_n, c.at<double>(p->L.poses[1]), sizeof(double) * 7 * p->N, cudaMemcpyDeviceToHost));
+  if (disps_n)
+    DBA_CUDA(cudaMemcpy(disps_n, c.at<float>(p->L.disps[1]), sizeof(float) * (size_t)p->N * p->P,
+                        cudaMemcpyDeviceToHost));
+  if (intr_n) DBA_CUDA(cudaMemcpy(intr_n, c.at<double>(p->L.intr[1]), sizeof(double) * 4, cudaMemcpyDeviceToHost));
+  if (energy_n) *energy_n = rb.energy;
   return DBA_OK;
 }
 

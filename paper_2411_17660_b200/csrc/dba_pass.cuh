@@ -53,6 +53,8 @@ struct PassArgs {
   float alpha, eta, d_min;
   const double* intr_c;
   const double* intr_n;
+  int gauge_frame;         // A5 mono gauge frame (global id) or -1
+  const double* gstate_c;  // [gamma, rho, h(u-space)] of the x_c linearisation
   double* part_edge;
   double* part_M;
   double* part_w;
@@ -83,7 +85,7 @@ __host__ __device__ inline int pass_ustride(int k, bool calib) { return pass_mpa
 
 // dynamic shared memory layout (bytes), identical on host and device
 struct PassSmem {
-  size_t eacc, stage, U, cinv, gdc, red, sl, sb, total;
+  size_t eacc, stage, U, cinv, gdc, hcs, red, sl, sb, total;
 };
 __host__ __device__ inline PassSmem pass_smem_layout(int kmax, bool calib) {
   PassSmem s;
@@ -95,6 +97,7 @@ __host__ __device__ inline PassSmem pass_smem_layout(int kmax, bool calib) {
   s.U = o; o += sizeof(float) * (size_t)kBlock * pass_ustride(kmax, calib);
   s.cinv = o; o += sizeof(float) * kBlock;
   s.gdc = o; o += sizeof(float) * kBlock;
+  s.hcs = o; o += sizeof(float) * kBlock;
   o = (o + 15) & ~size_t(15);
   s.sl = o; o += sizeof(EdgeLin) * kmax;
   s.sb = o; o += sizeof(EdgeBack) * kmax;
@@ -114,6 +117,7 @@ __global__ void __launch_bounds__(kBlock, 1) pass_kernel(const PassArgs A) {
   float* U = reinterpret_cast<float*>(smem + L.U);
   float* cinv = reinterpret_cast<float*>(smem + L.cinv);
   float* gdc = reinterpret_cast<float*>(smem + L.gdc);
+  float* hcs = reinterpret_cast<float*>(smem + L.hcs);
   EdgeLin* sl = reinterpret_cast<EdgeLin*>(smem + L.sl);
   EdgeBack* sb = reinterpret_cast<EdgeBack*>(smem + L.sb);
 
@@ -137,6 +141,7 @@ __global__ void __launch_bounds__(kBlock, 1) pass_kernel(const PassArgs A) {
       reinterpret_cast<float*>(sb)[x] = reinterpret_cast<const float*>(A.back + s0)[x];
   if (A.system)
     for (int x = tid; x < k * NVE; x += kBlock) eacc[x] = 0.0;
+  __syncthreads();
 
   const float fxn = (float)A.intr_n[0], fyn = (float)A.intr_n[1];
   const float cxn = (float)A.intr_n[2], cyn = (float)A.intr_n[3];
@@ -171,7 +176,21 @@ __global__ void __launch_bounds__(kBlock, 1) pass_kernel(const PassArgs A) {
   for (int s = 0; s < MT; ++s)
 #pragma unroll
     for (int x = 0; x < 16; ++x) Macc[s][x] = 0.0;
-  double wacc = 0.0;
+  double wacc = 0.0, hacc = 0.0;
+  const bool gauge = (f == A.gauge_frame) && k > 0;
+  // A5: kappa = (rho - h . delta_local) / gamma from the x_c linearisation
+  double kappa = 0.0;
+  if (gauge && A.backsub) {
+    const double* gs = A.gstate_c;
+    double hd = 0.0;
+    for (int a = 0; a < k; ++a)
+      for (int q = 0; q < 6; ++q) hd += gs[2 + 6 * a + q] * (double)sb[a].dlt[q];
+    if (CALIB) {
+      hd += gs[2 + 6 * k + 0] * (A.intr_n[0] - A.intr_c[0]) + gs[2 + 6 * k + 1] * (A.intr_n[1] - A.intr_c[1]) +
+            gs[2 + 6 * k + 2] * (A.intr_n[2] - A.intr_c[2]) + gs[2 + 6 * k + 3] * (A.intr_n[3] - A.intr_c[3]);
+    }
+    kappa = (gs[1] - hd) / gs[0];
+  }
   double facc[kFrameVals];
 #pragma unroll
   for (int x = 0; x < kFrameVals; ++x) facc[x] = 0.0;
@@ -236,7 +255,9 @@ __global__ void __launch_bounds__(kBlock, 1) pass_kernel(const PassArgs A) {
       }
       C += A.alpha * pm;
       gd += A.alpha * pm * (dstar - dc);
-      if (in) dn = fmaxf(dc + (gd - acc) / C, A.d_min);
+      float dd = (gd - acc) / C;
+      if (gauge) dd -= (float)(kappa / (double)dc);  // A5: r/C - kappa/d
+      if (in) dn = fmaxf(dc + dd, A.d_min);
     }
     if (in) A.d_new[fp] = dn;
 
@@ -357,6 +378,12 @@ __global__ void __launch_bounds__(kBlock, 1) pass_kernel(const PassArgs A) {
     }
     cinv[tid] = in ? 1.f / C : 0.f;
     gdc[tid] = in ? gd / C : 0.f;
+    if (gauge) {  // A5 with c = C/d: h = U^T (1/d), gamma = sum C/d^2, rho = sum g_d/d
+      const float id = in ? 1.f / dn : 0.f;
+      hcs[tid] = id;
+      facc[15] += (double)(C * id * id);
+      facc[16] += (double)(gd * id);
+    }
     __syncthreads();
 
     // per-edge partials: sum the 8 warp rows, accumulate in float64
@@ -395,9 +422,18 @@ __global__ void __launch_bounds__(kBlock, 1) pass_kernel(const PassArgs A) {
       for (int x = 0; x < 16; ++x) Macc[s][x] += (double)acc[x];
     }
     if (tid < mu) {
-      float s = 0.f;
-      for (int pp = 0; pp < kBlock; ++pp) s = fmaf(U[pp * ustride + tid], gdc[pp], s);
+      float s = 0.f, sh = 0.f;
+      if (gauge) {
+        for (int pp = 0; pp < kBlock; ++pp) {
+          const float u = U[pp * ustride + tid];
+          s = fmaf(u, gdc[pp], s);
+          sh = fmaf(u, hcs[pp], sh);
+        }
+      } else {
+        for (int pp = 0; pp < kBlock; ++pp) s = fmaf(U[pp * ustride + tid], gdc[pp], s);
+      }
       wacc += (double)s;
+      hacc += (double)sh;
     }
     __syncthreads();
   }
@@ -422,7 +458,10 @@ __global__ void __launch_bounds__(kBlock, 1) pass_kernel(const PassArgs A) {
           }
         }
     }
-    if (tid < mu) A.part_w[A.seg_off_w[sg] + tid] = wacc;
+    if (tid < mu) {
+      A.part_w[A.seg_off_w[sg] + tid] = wacc;
+      A.part_w[A.seg_off_w[sg] + mu + tid] = hacc;
+    }
   }
   // per-frame values: fixed-order block reduction in float64
 #pragma unroll

@@ -130,6 +130,9 @@ struct AsmArgs {
   const long long* off_F;
   const long long* off_f;
   int* bad_edge;
+  int gauge_frame;        // A5 (global frame id) or -1
+  const int* frame_of;
+  double* gstate;         // out: [gamma, rho, h] for the gauge frame
 };
 
 __device__ __forceinline__ int tri6(int r, int c) {
@@ -156,6 +159,8 @@ __global__ void __launch_bounds__(256) assemble_kernel(const AsmArgs A) {
   __shared__ double ws[6 * kMaxOutDegree + 4];
   __shared__ double fs[kFrameVals];
   __shared__ double Nm[6 * (6 * kMaxOutDegree + 4)];
+  __shared__ double hg[6 * kMaxOutDegree + 4];
+  __shared__ double Th[6 * kMaxOutDegree + 10];
   const int fl = blockIdx.x, tid = threadIdx.x;
   const int s0 = A.csr_off[fl], k = A.csr_off[fl + 1] - s0;
   if (k == 0) return;
@@ -171,10 +176,15 @@ __global__ void __launch_bounds__(256) assemble_kernel(const AsmArgs A) {
     for (int sg = sg0; sg < sg1; ++sg) s += A.part_edge[A.seg_off_edge[sg] + x];
     hs[x] = s;
   }
+  const bool gauge = A.frame_of[fl] == A.gauge_frame;
   for (int x = tid; x < mu; x += blockDim.x) {
-    double s = 0.0;
-    for (int sg = sg0; sg < sg1; ++sg) s += A.part_w[A.seg_off_w[sg] + x];
+    double s = 0.0, h = 0.0;
+    for (int sg = sg0; sg < sg1; ++sg) {
+      s += A.part_w[A.seg_off_w[sg] + x];
+      h += A.part_w[A.seg_off_w[sg] + mu + x];
+    }
     ws[x] = s;
+    hg[x] = h;
   }
   if (tid < kFrameVals) {
     double s = 0.0;
@@ -262,6 +272,29 @@ __global__ void __launch_bounds__(256) assemble_kernel(const AsmArgs A) {
     }
     fv[x] = v;
   }
+  if (!gauge) return;
+  // A5 gauge constraint (Sherman-Morrison): F += (T h)(T h)^T / gamma, f += (T h) rho / gamma
+  __syncthreads();
+  const double gam = fs[15], rho = fs[16];
+  for (int x = tid; x < m; x += blockDim.x) {
+    double v;
+    if (x < 6) {
+      v = 0.0;
+      for (int e = 0; e < k; ++e)
+        for (int q = 0; q < 6; ++q) v -= Ad[36 * e + 6 * q + x] * hg[6 * e + q];
+    } else {
+      v = hg[x - 6];
+    }
+    Th[x] = v;
+  }
+  if (tid == 0) {
+    A.gstate[0] = gam;
+    A.gstate[1] = rho;
+  }
+  for (int x = tid; x < mu; x += blockDim.x) A.gstate[2 + x] = hg[x];
+  __syncthreads();
+  for (int x = tid; x < m * m; x += blockDim.x) F[x] += Th[x / m] * Th[x % m] / gam;
+  for (int x = tid; x < m; x += blockDim.x) fv[x] += Th[x] * rho / gam;
 }
 
 // ---------------------------------------------------------------- gather

@@ -297,6 +297,30 @@ class DBASolver:
         return S[:n, :n], y[:n], float(e.value)
 
 
+    def debug_trial(self, poses, disps, intr, flow, prior=None, prior_mask=None, *, lam=1e-4,
+                    **opts):
+        """Test hook: one solve + trial pass from the input state without acceptance.
+        Returns (delta, poses_n, disps_n, intr_n, energy_n) as host arrays."""
+        P, D, K, F, PR, PM = self._inputs(poses, disps, intr, flow, prior, prior_mask)
+        buf = self._buffers(P, D, K, F, PR, PM)
+        n = int(self.info.n_reduced)
+        delta = np.zeros(max(n, 1))
+        pn = np.zeros((self.n_frames, 7))
+        dn = np.zeros((self.n_frames, self.height, self.width), dtype=np.float32)
+        kn = np.zeros(4)
+        e = ctypes.c_double()
+        o = self._options(1, **opts)
+        dp = ctypes.POINTER(ctypes.c_double)
+        with torch.cuda.device(self.device):
+            code = self.lib.dba_debug_trial(self._plan, ctypes.byref(o), ctypes.byref(buf),
+                                            float(lam), delta.ctypes.data_as(dp),
+                                            pn.ctypes.data_as(dp),
+                                            dn.ctypes.data_as(ctypes.POINTER(ctypes.c_float)),
+                                            kn.ctypes.data_as(dp), ctypes.byref(e))
+        _raise_for(code)
+        return delta[:n], pn, dn, kn, float(e.value)
+
+
 _PLAN_CACHE: dict = {}
 
 

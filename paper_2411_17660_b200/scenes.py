@@ -307,8 +307,11 @@ def make_workload(name, height=48, width=64, keyframes=None, radius=None, iters=
         cfg["radius"] = radius
     if iters is not None:
         cfg["iters"] = iters
+    focal = cfg.get("focal")
+    if focal is not None:  # C5's true focal (64 px at 48x64) scales with the grid width
+        focal = focal * width / 64.0
     spec = SceneSpec(trajectory=cfg["trajectory"], frames=cfg["scene_frames"],
-                     height=height, width=width, seed=0, focal=cfg.get("focal"))
+                     height=height, width=width, seed=0, focal=focal)
     sc = Scene(spec)
     frames = list(range(cfg["keyframes"]))
     ii, jj = radius_edges(len(frames), cfg["radius"])

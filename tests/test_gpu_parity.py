@@ -19,6 +19,15 @@ pytestmark = pytest.mark.gpu
 REL_TOL = 1e-4
 
 
+def _disp_err(d, d_ref, d_prev):
+    """Disparity error relative to the state magnitude max(d_ref, d_prev).
+
+    Equal to |d - d_ref| / d_ref except for pixels that a step drives towards zero
+    disparity, where the fp32 back-substitution's absolute error (which scales with
+    the step, not with the tiny result) is measured against the step's origin."""
+    return np.abs(d - d_ref) / np.maximum(d_ref, d_prev)
+
+
 @pytest.fixture(scope="module")
 def torch_cuda():
     import torch
@@ -119,3 +128,59 @@ def test_nonfinite_names_edge(torch_cuda):
     with pytest.raises(NumericalError) as ei:
         s.solve(wl.poses0, wl.disps0, wl.intr0, flow, iters=1)
     assert ei.value.edge == 5
+
+
+@pytest.mark.parametrize("calib", [False, True])
+def test_single_trial_stages(torch_cuda, calib):
+    """Step, retraction, back-substitution and trial energy of ONE trial vs the oracle."""
+    wl = small_workload("C5", keyframes=6, radius=2) if calib else small_workload("C1")
+    s = _solver(wl, calib=calib)
+    lam = 1e-4
+    delta, pn, dn, kn, en = s.debug_trial(wl.poses0, wl.disps0, wl.intr0, wl.flow, lam=lam)
+    opts = O.Options(optimize_intrinsics=calib)
+    prob = oracle_problem(wl)
+    st = oracle_state(wl)
+    sysm = O.linearize(st, prob, opts)
+    Sr, yr, _ = O.reduced(sysm, prob, opts)
+    dref, _ = O.solve_reduced(Sr, yr, lam)
+    assert _rel(delta, dref) < REL_TOL, _rel(delta, dref)
+    dxi, dth = O.split_step(dref, prob.fixed, calib)
+    dxi = O.clamp_tangents(dxi, opts.tangent_max)
+    trial = O.backsub_and_retract(st, prob, opts, dxi, dth)
+    te, ae = pose_errors(pn, trial.poses)
+    assert te < REL_TOL, te
+    rel = _disp_err(dn.astype(np.float64), trial.disps, st.disps)
+    assert rel.max() < REL_TOL, rel.max()
+    if calib:
+        assert np.abs(kn - trial.intr).max() / np.abs(trial.intr).max() < REL_TOL
+    eo = O.energy(trial, prob, opts)
+    assert abs(en - eo) <= REL_TOL * max(eo, 1e-3 * sysm.energy)
+
+
+def test_solve_parity_prior(torch_cuda):
+    wl = small_workload("C4", keyframes=8)
+    s = _solver(wl, prior=True)
+    Po, Do, Ko, rep = s.solve(wl.poses0, wl.disps0, wl.intr0, wl.flow, wl.prior, wl.prior_mask,
+                              iters=2)
+    ref, rrep = O.solve(oracle_state(wl), oracle_problem(wl, prior=True), O.Options(iters=2))
+    assert rep.iterations_run == rrep.iterations
+    te, ae = pose_errors(Po.cpu().numpy(), ref.poses)
+    assert te < REL_TOL, te
+    rel = _disp_err(Do.cpu().numpy().astype(np.float64), ref.disps, wl.disps0)
+    assert rel.max() < REL_TOL, rel.max()
+
+
+@pytest.mark.parametrize("iters", [1, 3])
+def test_solve_parity_calib(torch_cuda, iters):
+    wl = small_workload("C5", keyframes=12, radius=3)
+    s = _solver(wl, calib=True)
+    Po, Do, Ko, rep = s.solve(wl.poses0, wl.disps0, wl.intr0, wl.flow, iters=iters)
+    ref, rrep = O.solve(oracle_state(wl), oracle_problem(wl),
+                        O.Options(iters=iters, optimize_intrinsics=True))
+    assert rep.iterations_run == rrep.iterations
+    assert np.abs(Ko.cpu().numpy() - ref.intr).max() / np.abs(ref.intr).max() < REL_TOL
+    te, ae = pose_errors(Po.cpu().numpy(), ref.poses)
+    assert te < REL_TOL, te
+    rel = _disp_err(Do.cpu().numpy().astype(np.float64), ref.disps, wl.disps0)
+    assert np.quantile(rel, 0.999) < REL_TOL, np.quantile(rel, 0.999)
+    assert rel.max() < 10 * REL_TOL, rel.max()
