@@ -165,6 +165,20 @@ int dba_energy(dba_plan* plan, const dba_options* opt, const dba_buffers* buf,
 int dba_build_system(dba_plan* plan, const dba_options* opt, const dba_buffers* buf,
                      double* S_host, double* y_host, double* energy);
 
+/* Launch accounting and live kernel timing.  With profiling enabled the library
+ * brackets every fused-pass and solve launch with CUDA events on the launching
+ * stream and accumulates their durations (resolved at each per-trial sync). */
+typedef struct {
+  int64_t launches;        /* all kernels launched by the library */
+  int64_t pass_launches;   /* fused linearise/back-substitute passes */
+  int64_t solve_launches;  /* reduced-system factorisations */
+  double pass_ms;          /* summed CUDA-event time of the pass launches */
+  double solve_ms;         /* summed CUDA-event time of the solve launches */
+} dba_stats;
+
+int dba_plan_set_profiling(dba_plan* plan, int32_t enable);
+int dba_plan_get_stats(dba_plan* plan, dba_stats* stats, int32_t reset);
+
 /* Test hook: linearise at the input state, solve (S + lambda I) once, run one
  * trial pass, and return the step (n_reduced,), the trial poses (N,7), the
  * trial disparities (N,H,W) and intrinsics (4,) (all HOST) and the trial energy. */

@@ -75,10 +75,17 @@ class PlanInfo(ctypes.Structure):
     ]
 
 
+class Stats(ctypes.Structure):
+    _fields_ = [
+        ("launches", ctypes.c_int64), ("pass_launches", ctypes.c_int64),
+        ("solve_launches", ctypes.c_int64), ("pass_ms", c_dbl), ("solve_ms", c_dbl),
+    ]
+
+
 EXPORTS = (
     "dba_version", "dba_status_string", "dba_partition", "dba_plan_create", "dba_plan_destroy",
     "dba_plan_get_info", "dba_plan_local_edges", "dba_solve", "dba_energy", "dba_build_system",
-    "dba_debug_trial", "dba_nccl_unique_id", "dba_nccl_comm_init", "dba_nccl_comm_destroy",
+    "dba_plan_set_profiling", "dba_plan_get_stats", "dba_debug_trial", "dba_nccl_unique_id", "dba_nccl_comm_init", "dba_nccl_comm_destroy",
 )
 
 _lib = None
@@ -122,6 +129,10 @@ def load():
     lib.dba_energy.argtypes = [c_vp, P(Options), P(Buffers), P(c_dbl)]
     lib.dba_build_system.restype = c_i32
     lib.dba_build_system.argtypes = [c_vp, P(Options), P(Buffers), P(c_dbl), P(c_dbl), P(c_dbl)]
+    lib.dba_plan_set_profiling.restype = c_i32
+    lib.dba_plan_set_profiling.argtypes = [c_vp, c_i32]
+    lib.dba_plan_get_stats.restype = c_i32
+    lib.dba_plan_get_stats.argtypes = [c_vp, P(Stats), c_i32]
     lib.dba_debug_trial.restype = c_i32
     lib.dba_debug_trial.argtypes = [c_vp, P(Options), P(Buffers), c_dbl, P(c_dbl), P(c_dbl),
                                     P(ctypes.c_float), P(c_dbl), P(c_dbl)]

@@ -96,6 +96,15 @@ struct dba_plan {
   Readback* rb = nullptr;
   const void* uploaded_ws = nullptr;
   int device = -1;
+  // live kernel timing (dba_plan_set_profiling) and launch accounting
+  struct Prof {
+    bool on = false;
+    std::vector<cudaEvent_t> pool;
+    int used = 0;
+    std::vector<std::pair<int, int>> pass_ev, solve_ev;
+    long long launches = 0, pass_launches = 0, solve_launches = 0;
+    double pass_ms = 0.0, solve_ms = 0.0;
+  } prof;
 };
 
 namespace {
@@ -546,6 +555,7 @@ int dba_plan_create(const dba_problem_desc* d, dba_plan** out) {
 
 void dba_plan_destroy(dba_plan* p) {
   if (!p) return;
+  for (cudaEvent_t e : p->prof.pool) cudaEventDestroy(e);
   if (p->meta_pinned) cudaFreeHost(p->meta_pinned);
   if (p->rb) cudaFreeHost(p->rb);
   delete p;
@@ -590,6 +600,34 @@ struct Ctx {
     return reinterpret_cast<T*>(ws + off);
   }
 };
+
+int ev_pair(Ctx& c, std::pair<int, int>& out) {
+  auto& pr = c.p->prof;
+  while ((int)pr.pool.size() < pr.used + 2) {
+    cudaEvent_t e;
+    DBA_CUDA(cudaEventCreate(&e));
+    pr.pool.push_back(e);
+  }
+  out = {pr.used, pr.used + 1};
+  pr.used += 2;
+  return DBA_OK;
+}
+
+// accumulate the recorded event pairs (call after a stream synchronisation)
+void prof_resolve(dba_plan* p) {
+  auto& pr = p->prof;
+  for (auto& e : pr.pass_ev) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, pr.pool[e.first], pr.pool[e.second]) == cudaSuccess) pr.pass_ms += ms;
+  }
+  for (auto& e : pr.solve_ev) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, pr.pool[e.first], pr.pool[e.second]) == cudaSuccess) pr.solve_ms += ms;
+  }
+  pr.pass_ev.clear();
+  pr.solve_ev.clear();
+  pr.used = 0;
+}
 
 int check_args(dba_plan* p, const dba_options* o, const dba_buffers* b) {
   if (!p || !o || !b) return DBA_EINVAL;
@@ -643,6 +681,7 @@ int launch_prep(Ctx& c, int cur, int nxt, bool init) {
   a.adj = c.at<double>(p->L.adj);
   const int n = p->N + p->EL + 1;
   prep_kernel<<<(n + 127) / 128, 128, 0, c.st>>>(a);
+  p->prof.launches++;
   return cuda_status(cudaGetLastError());
 }
 
@@ -650,7 +689,19 @@ template <bool CALIB, int MT>
 int launch_pass_t(Ctx& c, const PassArgs& a) {
   auto k = pass_kernel<CALIB, MT>;
   DBA_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.p->pass_smem));
+  auto& pr = c.p->prof;
+  std::pair<int, int> ev{-1, -1};
+  if (pr.on) {
+    if (int s = ev_pair(c, ev)) return s;
+    DBA_CUDA(cudaEventRecord(pr.pool[ev.first], c.st));
+  }
   k<<<c.p->G, kBlock, c.p->pass_smem, c.st>>>(a);
+  pr.launches++;
+  pr.pass_launches++;
+  if (pr.on) {
+    DBA_CUDA(cudaEventRecord(pr.pool[ev.second], c.st));
+    pr.pass_ev.push_back(ev);
+  }
   return cuda_status(cudaGetLastError());
 }
 
@@ -728,6 +779,7 @@ int launch_system(Ctx& c, int slot) {
     a.frame_of = c.at<int>(p->L.frame_of);
     a.gstate = c.at<double>(p->L.gstate[slot]);
     assemble_kernel<<<p->NL, 256, 0, c.st>>>(a);
+    p->prof.launches++;
     DBA_CUDA(cudaGetLastError());
   }
   if (p->n_units > 0) {
@@ -740,6 +792,7 @@ int launch_system(Ctx& c, int slot) {
     g.sys = c.at<double>(p->L.sys[slot]);
     const int threads = 256, warps = threads / 32;
     gather_kernel<<<(p->n_units + warps - 1) / warps, threads, 0, c.st>>>(g);
+    p->prof.launches++;
     DBA_CUDA(cudaGetLastError());
   }
   FinalArgs f;
@@ -748,6 +801,7 @@ int launch_system(Ctx& c, int slot) {
   f.part_frame = c.at<double>(p->L.part_frame);
   f.energy_out = c.at<double>(p->L.sys[slot]) + p->energy_off;
   finalize_kernel<<<1, 256, 0, c.st>>>(f);
+  p->prof.launches++;
   DBA_CUDA(cudaGetLastError());
   if (c.comm && p->nranks > 1) {
     if (!nccl().ok) return DBA_ENCCL;
@@ -779,7 +833,19 @@ int launch_solve(Ctx& c, int slot, double lam) {
   a.cond = &c.at<Readback>(p->L.flags)->cond;
   DBA_CUDA(cudaFuncSetAttribute(solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)p->solve_smem));
+  auto& pr = p->prof;
+  std::pair<int, int> ev{-1, -1};
+  if (pr.on) {
+    if (int s2 = ev_pair(c, ev)) return s2;
+    DBA_CUDA(cudaEventRecord(pr.pool[ev.first], c.st));
+  }
   solve_kernel<<<1, kSolveThreads, p->solve_smem, c.st>>>(a);
+  pr.launches++;
+  pr.solve_launches++;
+  if (pr.on) {
+    DBA_CUDA(cudaEventRecord(pr.pool[ev.second], c.st));
+    pr.solve_ev.push_back(ev);
+  }
   return cuda_status(cudaGetLastError());
 }
 
@@ -802,6 +868,7 @@ int read_flags(Ctx& c, int slot, Readback& out) {
                            cudaMemcpyDeviceToHost, c.st));
   DBA_CUDA(cudaStreamSynchronize(c.st));
   out = *p->rb;
+  if (p->prof.on) prof_resolve(p);
   return DBA_OK;
 }
 
@@ -830,6 +897,7 @@ int gauge_sum(Ctx& c, const float* d, double* out) {
   const int g = p->gauge_frame;
   const int frame = (g >= p->f0 && g < p->f1) ? g : -1;
   logsum_kernel<<<1, 256, 0, c.st>>>(d, frame, p->P, out);
+  p->prof.launches++;
   DBA_CUDA(cudaGetLastError());
   if (c.comm && p->nranks > 1 && nccl().ok)
     if (nccl().AllReduce(out, out, 1, ncclDouble, ncclSum, c.comm, c.st) != ncclSuccess) return DBA_ENCCL;
@@ -928,11 +996,33 @@ int dba_solve(dba_plan* p, const dba_options* o, const dba_buffers* b, dba_repor
     g.poses = b->poses_out;
     const long long n = std::max<long long>((long long)p->NL * p->P, p->N);
     gauge_apply_kernel<<<(unsigned)((n + 255) / 256), 256, 0, c.st>>>(g);
+    p->prof.launches++;
     DBA_CUDA(cudaGetLastError());
     DBA_CUDA(cudaMemcpyAsync(&rep->scale, gsum + 2, sizeof(double), cudaMemcpyDeviceToHost, c.st));
   }
   DBA_CUDA(cudaStreamSynchronize(c.st));
+  if (p->prof.on) prof_resolve(p);
   rep->status = DBA_OK;
+  return DBA_OK;
+}
+
+int dba_plan_set_profiling(dba_plan* p, int32_t enable) {
+  if (!p) return DBA_EINVAL;
+  p->prof.on = enable != 0;
+  return DBA_OK;
+}
+
+int dba_plan_get_stats(dba_plan* p, dba_stats* st, int32_t reset) {
+  if (!p || !st) return DBA_EINVAL;
+  st->launches = p->prof.launches;
+  st->pass_launches = p->prof.pass_launches;
+  st->solve_launches = p->prof.solve_launches;
+  st->pass_ms = p->prof.pass_ms;
+  st->solve_ms = p->prof.solve_ms;
+  if (reset) {
+    p->prof.launches = p->prof.pass_launches = p->prof.solve_launches = 0;
+    p->prof.pass_ms = p->prof.solve_ms = 0.0;
+  }
   return DBA_OK;
 }
 

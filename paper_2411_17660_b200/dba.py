@@ -297,6 +297,17 @@ class DBASolver:
         return S[:n, :n], y[:n], float(e.value)
 
 
+    def set_profiling(self, enable=True):
+        """Bracket every pass/solve launch with CUDA events (live kernel timing)."""
+        _raise_for(self.lib.dba_plan_set_profiling(self._plan, int(bool(enable))))
+
+    def stats(self, reset=False):
+        st = _lib.Stats()
+        _raise_for(self.lib.dba_plan_get_stats(self._plan, ctypes.byref(st), int(bool(reset))))
+        return {"launches": st.launches, "pass_launches": st.pass_launches,
+                "solve_launches": st.solve_launches, "pass_ms": st.pass_ms,
+                "solve_ms": st.solve_ms}
+
     def debug_trial(self, poses, disps, intr, flow, prior=None, prior_mask=None, *, lam=1e-4,
                     **opts):
         """Test hook: one solve + trial pass from the input state without acceptance.
