@@ -289,7 +289,7 @@ int dba_plan_create(const dba_problem_desc* d, dba_plan** out) {
   {
     const SolveSmem s = solve_smem_layout(p->nb, p->BW, p->calib);
     p->solve_smem = s.total;
-    if (p->solve_smem > 200 * 1024) {
+    if (p->solve_smem > 200 * 1024 || p->BW > kMaxBand) {
       delete p;
       return DBA_ECAPACITY;
     }
@@ -831,15 +831,15 @@ int launch_solve(Ctx& c, int slot, double lam) {
   a.Lband = c.at<double>(p->L.Lband);
   a.delta = c.at<double>(p->L.delta);
   a.cond = &c.at<Readback>(p->L.flags)->cond;
-  DBA_CUDA(cudaFuncSetAttribute(solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)p->solve_smem));
+  auto kern = (p->BW <= 5) ? solve_kernel<1> : (p->BW <= 10) ? solve_kernel<2> : solve_kernel<5>;
+  DBA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->solve_smem));
   auto& pr = p->prof;
   std::pair<int, int> ev{-1, -1};
   if (pr.on) {
     if (int s2 = ev_pair(c, ev)) return s2;
     DBA_CUDA(cudaEventRecord(pr.pool[ev.first], c.st));
   }
-  solve_kernel<<<1, kSolveThreads, p->solve_smem, c.st>>>(a);
+  kern<<<1, kSolveThreads, p->solve_smem, c.st>>>(a);
   pr.launches++;
   pr.solve_launches++;
   if (pr.on) {
