@@ -296,14 +296,13 @@ int dba_plan_create(const dba_problem_desc* d, dba_plan** out) {
   }
 
   // ---- pass decomposition: G CTAs over (frame, 256-px tile) work items
-  p->n_tiles = (p->P + kBlock - 1) / kBlock;
+  p->n_tiles = (p->P + kSub - 1) / kSub;
   {
     const PassSmem s = pass_smem_layout(std::max(p->kmax, 1), p->calib);
     p->pass_smem = s.total;
     const int mpad = pass_mpad(std::max(p->kmax, 1), p->calib);
     const int nt = mpad / 4, ntiles = nt * (nt + 1) / 2;
-    p->MT = ntiles <= kBlock ? 1 : (ntiles <= 2 * kBlock ? 2 : 4);
-    if (p->pass_smem > 220 * 1024 || p->MT > 2) {
+    if (p->pass_smem > 225 * 1024 || ntiles > kPassThreads) {
       delete p;
       return DBA_ECAPACITY;
     }
@@ -314,9 +313,8 @@ int dba_plan_create(const dba_problem_desc* d, dba_plan** out) {
     if (cudaGetDeviceProperties(&prop, dev) == cudaSuccess) sms = prop.multiProcessorCount;
   }
   p->device = dev;
-  const int per_sm = std::max(1, std::min(2, (int)((227 * 1024) / std::max<size_t>(p->pass_smem, 1))));
   const long long items = (long long)p->NL * p->n_tiles;
-  p->G = (int)std::max<long long>(1, std::min<long long>(items, (long long)sms * per_sm));
+  p->G = (int)std::max<long long>(1, std::min<long long>(items, (long long)sms));  // one 512-thread CTA per SM
   // weighted contiguous split, cost of a tile ~ (out-degree + 2)
   std::vector<int> seg_frame, seg_t0, seg_t1, cta_seg(p->G + 1, 0), frame_seg(p->NL + 1, 0);
   {
@@ -685,9 +683,9 @@ int launch_prep(Ctx& c, int cur, int nxt, bool init) {
   return cuda_status(cudaGetLastError());
 }
 
-template <bool CALIB, int MT>
+template <bool CALIB>
 int launch_pass_t(Ctx& c, const PassArgs& a) {
-  auto k = pass_kernel<CALIB, MT>;
+  auto k = pass_kernel<CALIB>;
   DBA_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.p->pass_smem));
   auto& pr = c.p->prof;
   std::pair<int, int> ev{-1, -1};
@@ -695,7 +693,7 @@ int launch_pass_t(Ctx& c, const PassArgs& a) {
     if (int s = ev_pair(c, ev)) return s;
     DBA_CUDA(cudaEventRecord(pr.pool[ev.first], c.st));
   }
-  k<<<c.p->G, kBlock, c.p->pass_smem, c.st>>>(a);
+  k<<<c.p->G, kPassThreads, c.p->pass_smem, c.st>>>(a);
   pr.launches++;
   pr.pass_launches++;
   if (pr.on) {
@@ -745,12 +743,8 @@ int launch_pass(Ctx& c, int cur, int nxt, bool backsub, bool system) {
   a.seg_off_edge = c.at<long long>(p->L.seg_off_edge);
   a.seg_off_M = c.at<long long>(p->L.seg_off_M);
   a.seg_off_w = c.at<long long>(p->L.seg_off_w);
-  if (p->calib) {
-    if (p->MT == 1) return launch_pass_t<true, 1>(c, a);
-    return launch_pass_t<true, 2>(c, a);
-  }
-  if (p->MT == 1) return launch_pass_t<false, 1>(c, a);
-  return launch_pass_t<false, 2>(c, a);
+  if (p->calib) return launch_pass_t<true>(c, a);
+  return launch_pass_t<false>(c, a);
 }
 
 int launch_system(Ctx& c, int slot) {
