@@ -300,8 +300,7 @@ int dba_plan_create(const dba_problem_desc* d, dba_plan** out) {
   {
     const PassSmem s = pass_smem_layout(std::max(p->kmax, 1), p->calib);
     p->pass_smem = s.total;
-    const int mpad = pass_mpad(std::max(p->kmax, 1), p->calib);
-    const int nt = mpad / 4, ntiles = nt * (nt + 1) / 2;
+    const int ntiles = pass_ntiles(pass_mpad(std::max(p->kmax, 1), p->calib));
     if (p->pass_smem > 225 * 1024 || ntiles > kPassThreads) {
       delete p;
       return DBA_ECAPACITY;
@@ -1047,6 +1046,7 @@ int dba_build_system(dba_plan* p, const dba_options* o, const dba_buffers* b, do
   DBA_CUDA(cudaMemcpyAsync(sys.data(), c.at<double>(p->L.sys[0]), sizeof(double) * p->sys_len,
                            cudaMemcpyDeviceToHost, c.st));
   DBA_CUDA(cudaStreamSynchronize(c.st));
+  if (p->prof.on) prof_resolve(p);
   const int n = p->n_red, W1 = p->BW + 1;
   std::fill(S, S + (size_t)n * n, 0.0);
   for (int a = 0; a < p->nb; ++a)

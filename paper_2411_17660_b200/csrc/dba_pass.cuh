@@ -12,12 +12,12 @@
 //       d_n = max(d + delta d, d_min)
 //   phase B (linearisation at x_n = trial state), edge-major:
 //       residual, validity (geometry.py:235-250), J_j, J_d, [J_theta];
-//       energy, per-edge H_jj / g_j accumulated in REGISTERS of the warp that
-//       owns the unit for the whole segment (one warp reduction per segment);
+//       energy, per-edge H_jj / g_j accumulated in registers of the warp that
+//       owns the units (one warp transpose-reduce per edge per sub-tile);
 //       E_e,p -> shared U[p][6e..6e+5]; per-edge parts of C_p, g_d,p
 //   per pixel: C_p, g_d,p (+ Eq. 4 prior), U[p] row extended by [g_d,p, C_p/d_p]
-//   phase C (K3a): M_ext += U_ext^T diag(1/C) U_ext, a shared-memory SIMT GEMM
-//       split over pixels across warp groups.  The two extra rows give, in the
+//   phase C (K3a): M_ext += V V^T with V = U_ext / sqrt(C), a shared-memory SIMT
+//       GEMM in 4x8 register tiles split over pixels across warp groups.  The two extra rows give, in the
 //       same GEMM, w = E C^-1 g_d (Schur rhs) and the A5 gauge terms
 //       h = E C^-1 c, rho = c^T C^-1 g_d, gamma = c^T C^-1 c with c = C/d.
 //
@@ -92,13 +92,22 @@ __device__ __forceinline__ float transpose_reduce32(float (&v)[32], int lane) {
 }
 
 __host__ __device__ inline int pass_mu(int k, bool calib) { return 6 * k + (calib ? 4 : 0); }
-// GEMM rows: U (mu) + [g_d, C/d], padded to a multiple of 4
+// GEMM rows: U (mu) + [g_d, C/d], padded to a multiple of 8 (4x8 register tiles)
 __host__ __device__ inline int pass_mext(int k, bool calib) { return pass_mu(k, calib) + 2; }
-__host__ __device__ inline int pass_mpad(int k, bool calib) { return (pass_mext(k, calib) + 3) & ~3; }
+__host__ __device__ inline int pass_mpad(int k, bool calib) { return (pass_mext(k, calib) + 7) & ~7; }
+// row stride = 2 (mod 8): float2 accesses by 16 lanes of consecutive pixel rows are
+// conflict-free; the GEMM reads rows with 8-byte loads
 __host__ __device__ inline int pass_ustride(int k, bool calib) { return pass_mpad(k, calib) + 2; }
+// number of 4x8 tiles touching the upper triangle of an (mpad x mpad) matrix
+__host__ __device__ inline int pass_ntiles(int mpad) {
+  const int nr = mpad / 4, nc = mpad / 8;
+  int n = 0;
+  for (int tj = 0; tj < nc; ++tj) n += (2 * tj + 2 < nr) ? 2 * tj + 2 : nr;
+  return n;
+}
 
 struct PassSmem {
-  size_t U, parts, dcs, dns, cinv, ebuf, ethb, red, emap, sflow, sl, sb, total;
+  size_t U, parts, dcs, dns, qc, qn, ebuf, ethb, red, emap, sflow, sl, sb, total;
 };
 __host__ __device__ inline PassSmem pass_smem_layout(int kmax, bool calib) {
   PassSmem s;
@@ -107,17 +116,17 @@ __host__ __device__ inline PassSmem pass_smem_layout(int kmax, bool calib) {
   s.ethb = o; o += calib ? sizeof(double) * kPassWarps * kEdgeSlots * 32 : 0;
   s.red = o; o += sizeof(double) * kPassWarps * 16;
   s.U = o; o += sizeof(float) * (size_t)kSub * pass_ustride(kmax, calib);
-  {  // the segment-end M reduction reuses U: needs 16 doubles per tile
-    const int nt = pass_mpad(kmax, calib) / 4;
-    const size_t need = sizeof(double) * 16 * (size_t)(nt * (nt + 1) / 2);
+  {  // the segment-end GEMM partials reuse U: 32 floats per thread
+    const size_t need = sizeof(float) * 32 * kPassThreads;
     const size_t have = sizeof(float) * (size_t)kSub * pass_ustride(kmax, calib);
     if (need > have) o += need - have;
   }
   s.parts = o; o += sizeof(float) * (size_t)nparts * kmax * kSub;
   s.dcs = o; o += sizeof(float) * kSub;
   s.dns = o; o += sizeof(float) * kSub;
-  s.cinv = o; o += sizeof(float) * kSub;
-  s.ebuf = o; o += sizeof(float) * kPassWarps * kEdgeSlots * 32;
+  s.qc = o; o += sizeof(float2) * kSub;
+  s.qn = o; o += sizeof(float2) * kSub;
+  s.ebuf = o; o += sizeof(double) * kPassWarps * kEdgeSlots * 32;
   s.emap = o; o += sizeof(int) * kPassWarps * kEdgeSlots;
   s.sflow = o; o += sizeof(int) * kmax;
   o = (o + 15) & ~size_t(15);
@@ -161,12 +170,13 @@ __global__ void __launch_bounds__(kPassThreads, 1) pass_kernel(const PassArgs A)
   constexpr int NVE = kEdgeVals + (CALIB ? kCalibVals : 0);
   const PassSmem L = pass_smem_layout(A.kmax, CALIB);
   float* U = reinterpret_cast<float*>(smem + L.U);
-  double* Mred = reinterpret_cast<double*>(smem + L.U);  // segment end only
+  float* Mg = reinterpret_cast<float*>(smem + L.U);  // segment end only: [32][kPassThreads]
   float* parts = reinterpret_cast<float*>(smem + L.parts);
   float* dcs = reinterpret_cast<float*>(smem + L.dcs);
   float* dns = reinterpret_cast<float*>(smem + L.dns);
-  float* cinv = reinterpret_cast<float*>(smem + L.cinv);
-  float* ebuf = reinterpret_cast<float*>(smem + L.ebuf);
+  float2* qcs = reinterpret_cast<float2*>(smem + L.qc);  // normalised pixel rays at x_c
+  float2* qns = reinterpret_cast<float2*>(smem + L.qn);  // ... at x_n
+  double* ebuf = reinterpret_cast<double*>(smem + L.ebuf);
   double* ethb = reinterpret_cast<double*>(smem + L.ethb);
   double* red = reinterpret_cast<double*>(smem + L.red);
   int* emap = reinterpret_cast<int*>(smem + L.emap);
@@ -191,7 +201,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) pass_kernel(const PassArgs A)
     const int f = A.frame_of[fl];
     const int mu = pass_mu(k, CALIB);
     const int mext = mu + 2;
-    const int mpad = (mext + 3) & ~3;
+    const int mpad = (mext + 7) & ~7;
     const int ustride = mpad + 2;
     float* Pa0 = parts;                  // [k][kSub]  C part
     float* Pa1 = parts + KM * kSub;      // [k][kSub]  g_d part
@@ -212,30 +222,32 @@ __global__ void __launch_bounds__(kPassThreads, 1) pass_kernel(const PassArgs A)
       const int e = e0 + lane;
       emap[warp * kEdgeSlots + lane] = (u1 > u0 && e * kSlices < u1 && e < k) ? e : -1;
     }
-    if (CALIB)
-      for (int x = tid; x < kPassWarps * kEdgeSlots * 32; x += kPassThreads) ethb[x] = 0.0;
-    // GEMM assignment: upper 4x4 tiles x pixel groups
-    const int nt = mpad >> 2;
-    const int ntiles = nt * (nt + 1) / 2;
-    const int G = A.system ? max(1, min(8, kPassThreads / max(ntiles, 1))) : 0;
+    for (int x = tid; x < kPassWarps * kEdgeSlots * 32; x += kPassThreads) {
+      ebuf[x] = 0.0;
+      if (CALIB) ethb[x] = 0.0;
+    }
+    // GEMM assignment: 4x8 tiles touching the upper triangle x pixel groups
+    const int nr = mpad >> 2;
+    const int ntiles = pass_ntiles(mpad);
+    const int G = A.system ? max(1, min(16, kPassThreads / max(ntiles, 1))) : 0;
     int tI = -1, tJ = -1, gk0 = 0, gk1 = 0;
     if (A.system && tid < G * ntiles) {
       int t = tid % ntiles;
       const int g = tid / ntiles;
-      int r = 0;
-      while (t >= nt - r) {
-        t -= nt - r;
-        ++r;
+      int tj = 0;
+      while (t >= min(2 * tj + 2, nr)) {
+        t -= min(2 * tj + 2, nr);
+        ++tj;
       }
-      tI = r;
-      tJ = r + t;
+      tI = t;
+      tJ = tj;
       gk0 = (kSub * g) / G;
       gk1 = (kSub * (g + 1)) / G;
     }
-    float Macc[16];
+    float Macc[32];
 #pragma unroll
-    for (int x = 0; x < 16; ++x) Macc[x] = 0.f;
-    float hacc[kEdgeSlots][28];
+    for (int x = 0; x < 32; ++x) Macc[x] = 0.f;
+    float hacc[kEdgeSlots][28];  // per-edge H_jj, g_j, energy of this warp's units (whole segment)
 #pragma unroll
     for (int s = 0; s < kEdgeSlots; ++s)
 #pragma unroll
@@ -262,10 +274,14 @@ __global__ void __launch_bounds__(kPassThreads, 1) pass_kernel(const PassArgs A)
       if (tid < kSub) {
         const int p = pbase + tid;
         dcs[tid] = p < P ? A.d_cur[(size_t)f * P + p] : 1.f;
+        const float pu = (float)(p % A.W), pv = (float)(p / A.W);
+        qcs[tid] = make_float2((pu - cxc) / fxc, (pv - cyc) / fyc);
+        qns[tid] = make_float2((pu - cxn) / fxn, (pv - cyn) / fyn);
       }
       __syncthreads();
       // ------------------------------------------------------------ phase A
       if (A.backsub) {
+#ifndef DBA_PASS_SKIP_A
         for (int u = u0; u < u1; ++u) {
           const int a = u / kSlices, sl0 = (u % kSlices) * kSlice;
           const EdgeBack& e = sb[a];
@@ -276,7 +292,8 @@ __global__ void __launch_bounds__(kPassThreads, 1) pass_kernel(const PassArgs A)
             const bool in = p < P;
             const float4 fw = in ? __ldg(fl4 + p) : make_float4(0.f, 0.f, 0.f, 0.f);
             const float dc = dcs[pl];
-            const float qx = ((float)(p % A.W) - cxc) / fxc, qy = ((float)(p / A.W) - cyc) / fyc;
+            const float2 q = qcs[pl];
+            const float qx = q.x, qy = q.y;
             const PixTerms T = pix_terms(e.R, e.t, qx, qy, dc, fxc, fyc, cxc, cyc, Wf, Hf, fw, in);
             const float fxi = fxc * T.iz, fyi = fyc * T.iz;
             const float Jdu = fxi * (e.t[0] - T.xt * e.t[2]);
@@ -300,6 +317,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) pass_kernel(const PassArgs A)
             Pa2[a * kSub + pl] = fmaf(au, ju, av * jv);
           }
         }
+#endif
         __syncthreads();
         if (tid < kSub) {
           const int p = pbase + tid;
@@ -333,7 +351,11 @@ __global__ void __launch_bounds__(kPassThreads, 1) pass_kernel(const PassArgs A)
       }
       __syncthreads();
       // ------------------------------------------------------------ phase B
+#ifdef DBA_PASS_SKIP_B
+      for (int u = u0; u < u0; ++u) {
+#else
       for (int u = u0; u < u1; ++u) {
+#endif
         const int a = u / kSlices, sl0 = (u % kSlices) * kSlice;
         const int slot = a - e0;
         const EdgeLin& e = sl[a];
@@ -349,7 +371,8 @@ __global__ void __launch_bounds__(kPassThreads, 1) pass_kernel(const PassArgs A)
           const bool in = p < P;
           const float4 fw = in ? __ldg(fl4 + p) : make_float4(0.f, 0.f, 0.f, 0.f);
           const float dn = dns[pl];
-          const float qx = ((float)(p % A.W) - cxn) / fxn, qy = ((float)(p / A.W) - cyn) / fyn;
+          const float2 q = qns[pl];
+          const float qx = q.x, qy = q.y;
           const PixTerms T = pix_terms(e.R, e.t, qx, qy, dn, fxn, fyn, cxn, cyn, Wf, Hf, fw, in);
           const float en = T.wu * T.ru * T.ru + T.wv * T.rv * T.rv;
           facc[0] += en;
@@ -469,52 +492,44 @@ __global__ void __launch_bounds__(kPassThreads, 1) pass_kernel(const PassArgs A)
             U2[0] = make_float2(Et[0], Et[1]);
             U2[1] = make_float2(Et[2], Et[3]);
           }
-          Urow[mu] = in ? gd : 0.f;
-          Urow[mu + 1] = in ? C / dn : 0.f;  // A5 with c = C/d (only the gauge frame uses it)
-          for (int c = mext; c < mpad; ++c) Urow[c] = 0.f;
-          if (!in)
-            for (int c = 0; c < mu; ++c) Urow[c] = 0.f;
-          cinv[tid] = in ? 1.f / C : 0.f;
+          // V = U_ext / sqrt(C): the GEMM below is then M_ext = V V^T
+          const float sq = in ? rsqrtf(C) : 0.f;
+          float2* U2 = reinterpret_cast<float2*>(Urow);
+          for (int c = 0; c < (mu >> 1); ++c) {  // mu is even
+            const float2 v = U2[c];
+            U2[c] = make_float2(v.x * sq, v.y * sq);
+          }
+          U2[mu >> 1] = make_float2(gd * sq, in ? C / dn * sq : 0.f);  // A5 with c = C/d
+          for (int c = (mext >> 1); c < (mpad >> 1); ++c) U2[c] = make_float2(0.f, 0.f);
         }
       }
       __syncthreads();
       if (!A.system) continue;
       // ------------------------------------------------------------ phase C (K3a)
+#ifdef DBA_PASS_SKIP_GEMM
+      if (tI >= 0 && tI < -1) {
+#else
       if (tI >= 0) {
-        float acc[16];
-#pragma unroll
-        for (int x = 0; x < 16; ++x) acc[x] = 0.f;
-        const int ca = 4 * tI, cb = 4 * tJ;
-#pragma unroll 4
+#endif
+        const int ca = 4 * tI, cb = 8 * tJ;
+#pragma unroll 2
         for (int pp = gk0; pp < gk1; ++pp) {
-          const float* row = U + pp * ustride;
-          const float2 a01 = *reinterpret_cast<const float2*>(row + ca);
-          const float2 a23 = *reinterpret_cast<const float2*>(row + ca + 2);
-          const float2 b01 = *reinterpret_cast<const float2*>(row + cb);
-          const float2 b23 = *reinterpret_cast<const float2*>(row + cb + 2);
-          const float ci = cinv[pp];
-          const float av4[4] = {a01.x, a01.y, a23.x, a23.y};
-          const float bv4[4] = {b01.x * ci, b01.y * ci, b23.x * ci, b23.y * ci};
+          const float2* row = reinterpret_cast<const float2*>(U + pp * ustride);
+          const float2 a0 = row[(ca >> 1)], a1 = row[(ca >> 1) + 1];
+          const float2 b0 = row[(cb >> 1)], b1 = row[(cb >> 1) + 1], b2 = row[(cb >> 1) + 2],
+                       b3 = row[(cb >> 1) + 3];
+          const float av[4] = {a0.x, a0.y, a1.x, a1.y};
+          const float bv[8] = {b0.x, b0.y, b1.x, b1.y, b2.x, b2.y, b3.x, b3.y};
 #pragma unroll
           for (int r = 0; r < 4; ++r)
 #pragma unroll
-            for (int c = 0; c < 4; ++c) acc[4 * r + c] = fmaf(av4[r], bv4[c], acc[4 * r + c]);
+            for (int c = 0; c < 8; ++c) Macc[8 * r + c] = fmaf(av[r], bv[c], Macc[8 * r + c]);
         }
-#pragma unroll
-        for (int x = 0; x < 16; ++x) Macc[x] += acc[x];
       }
       __syncthreads();
     }
 
     // ------------------------------------------------------------ segment outputs
-    // per-frame values: fixed-order block reduction (float64 across warps)
-#pragma unroll
-    for (int x = 0; x < 15; ++x) {
-      float v = facc[x];
-#pragma unroll
-      for (int off = 16; off >= 1; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-      if (lane == 0) red[warp * 16 + x] = (double)v;
-    }
     if (A.system) {
       // per-edge register accumulators: one transpose-reduce per slot per segment
 #pragma unroll
@@ -525,8 +540,21 @@ __global__ void __launch_bounds__(kPassThreads, 1) pass_kernel(const PassArgs A)
 #pragma unroll
         for (int x = 28; x < 32; ++x) v32[x] = 0.f;
         const float rs = transpose_reduce32(v32, lane);
-        ebuf[(warp * kEdgeSlots + s) * 32 + lane] = rs;
+        ebuf[(warp * kEdgeSlots + s) * 32 + lane] = (double)rs;
       }
+      // GEMM partials of every (tile, pixel group) thread -> Mg[x][tid] (aliases U)
+      if (tI >= 0) {
+#pragma unroll
+        for (int x = 0; x < 32; ++x) Mg[x * kPassThreads + tid] = Macc[x];
+      }
+    }
+    // per-frame values: fixed-order block reduction (float64 across warps)
+#pragma unroll
+    for (int x = 0; x < 15; ++x) {
+      float v = facc[x];
+#pragma unroll
+      for (int off = 16; off >= 1; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+      if (lane == 0) red[warp * 16 + x] = (double)v;
     }
     __syncthreads();
     double* pf = A.part_frame + (long long)sg * kFrameVals;
@@ -542,27 +570,23 @@ __global__ void __launch_bounds__(kPassThreads, 1) pass_kernel(const PassArgs A)
         const int a = x / NVE, l = x % NVE;
         double v = 0.0;
         for (int ws = 0; ws < kPassWarps * kEdgeSlots; ++ws)
-          if (emap[ws] == a) v += (l < 32) ? (double)ebuf[ws * 32 + l] : ethb[ws * 32 + (l - 32)];
+          if (emap[ws] == a) v += (l < 32) ? ebuf[ws * 32 + l] : ethb[ws * 32 + (l - 32)];
         pe[x] = v;
       }
-      // M_ext: sum the pixel groups in fixed order (Mred aliases U, free now)
-      for (int g = 0; g < G; ++g) {
-        if (tI >= 0 && tid / ntiles == g) {
-          const int t = tid % ntiles;
-#pragma unroll
-          for (int x = 0; x < 16; ++x) Mred[16 * t + x] = (g == 0 ? 0.0 : Mred[16 * t + x]) + (double)Macc[x];
-        }
-        __syncthreads();
-      }
-      // unpack: M (mu x mu), w = column mu, h = column mu+1, rho, gamma
+      // unpack: M (mu x mu), w = column mu, h = column mu+1, rho, gamma;
+      // each entry sums its tile's pixel groups in fixed order (float64)
       double* pM = A.part_M + A.seg_off_M[sg];
       double* pw = A.part_w + A.seg_off_w[sg];
       for (int x = tid; x < mext * mext; x += kPassThreads) {
         const int R = x / mext, Cc = x % mext;
         const int lo = min(R, Cc), hi = max(R, Cc);
-        const int ti = lo >> 2, tj = hi >> 2;
-        const int t = ti * nt - ti * (ti - 1) / 2 + (tj - ti);
-        const double v = Mred[16 * t + 4 * (lo & 3) + (hi & 3)];
+        const int ti = lo >> 2, tj = hi >> 3;
+        // tiles are enumerated column block by column block: sum_{j<tj} min(2j+2, nr)
+        const int full = min(tj, (nr - 1) / 2);  // blocks with 2j+2 <= nr
+        const int t = ti + full * (full + 1) + (tj - full) * nr;
+        const int e = 8 * (lo & 3) + (hi & 7);
+        double v = 0.0;
+        for (int g = 0; g < G; ++g) v += (double)Mg[e * kPassThreads + g * ntiles + t];
         if (R < mu && Cc < mu)
           pM[(long long)R * mu + Cc] = v;
         else if (R < mu && Cc == mu)
