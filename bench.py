@@ -180,9 +180,9 @@ def run_reference(args):
         return
     steps = []
     for _ in range(args.warmup):
-        cpu_baseline(1, sample_frames=12)
+        cpu_baseline(1, sample_frames=24)
     for _ in range(args.steps):
-        steps.append(cpu_baseline(1, sample_frames=12))
+        steps.append(cpu_baseline(1, sample_frames=24))
     v = statistics.median(s["value"] for s in steps)
     cb = dict(steps[-1])
     cb["value"] = v
