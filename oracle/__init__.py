@@ -12,8 +12,9 @@ geometry   float64 numpy restatement of ``/root/reference/pkg/src/flowsplat/geom
            (pinned against the reference's own tests + golden vectors in tests/golden).
 dba        float64 restatement of the SPEC's dense bundle adjustment
            (``/root/reference/SPEC.md:286-394``).  The reference ships NO dba
-           module (``__init__.py:8`` names it, the file is absent), so DBA parity
-           is pinned by the SPEC's own properties (finite-difference Jacobians,
+           module (``__init__.py:8`` names it, the file is absent): DBA parity is
+           UNPINNED by reference code ("parity unpinned"); it is pinned by the
+           SPEC's own properties (finite-difference Jacobians,
            Schur == dense joint solve, zero energy at truth, fixed point at
            truth, monotone energy, 8-keyframe recovery) — see DESIGN.md §Oracle.
 sharded    the same algorithm over a frame partition (partial systems summed),
