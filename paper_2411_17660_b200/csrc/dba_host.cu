@@ -84,7 +84,7 @@ struct dba_plan {
   int N = 0, H = 0, W = 0, P = 0, E = 0;
   int calib = 0, prior = 0, gauge_on = 0, gauge_frame = -1, rank = 0, nranks = 1;
   int f0 = 0, f1 = 0, NL = 0, EL = 0, kmax = 0, nb = 0, BW = 0, n_red = 0;
-  int n_tiles = 0, G = 0, nseg = 0, n_units = 0, nve = kEdgeVals, MT = 1;
+  int n_tiles = 0, G = 0, nseg = 0, n_units = 0, nve = kEdgeVals, stage = 1;
   size_t pass_smem = 0, solve_smem = 0;
   long long sys_len = 0;  // doubles in one packed reduced system
   long long band_len = 0, theta_off = 0, thth_off = 0, y_off = 0, energy_off = 0;
@@ -298,7 +298,12 @@ int dba_plan_create(const dba_problem_desc* d, dba_plan** out) {
   // ---- pass decomposition: G CTAs over (frame, 256-px tile) work items
   p->n_tiles = (p->P + kSub - 1) / kSub;
   {
-    const PassSmem s = pass_smem_layout(std::max(p->kmax, 1), p->calib);
+    PassSmem s = pass_smem_layout(std::max(p->kmax, 1), p->calib, true);
+    p->stage = 1;
+    if (s.total > 225 * 1024) {  // no room to stage the flow records: read them from L2
+      s = pass_smem_layout(std::max(p->kmax, 1), p->calib, false);
+      p->stage = 0;
+    }
     p->pass_smem = s.total;
     const int ntiles = pass_ntiles(pass_mpad(std::max(p->kmax, 1), p->calib));
     if (p->pass_smem > 225 * 1024 || ntiles > kPassThreads) {
@@ -713,6 +718,7 @@ int launch_pass(Ctx& c, int cur, int nxt, bool backsub, bool system) {
   a.kmax = std::max(p->kmax, 1);
   a.backsub = backsub ? 1 : 0;
   a.system = system ? 1 : 0;
+  a.stage = p->stage;
   a.status = c.at<int>(p->L.flags);
   a.csr_off = c.at<int>(p->L.csr_off);
   a.slot_flow = c.at<int>(p->L.slot_flow);

@@ -47,6 +47,7 @@ struct PassArgs {
   int H, W, P, n_tiles, kmax;
   int backsub;  // run phase A
   int system;   // produce system partials (0: energy only)
+  int stage;    // flow records of the next sub-tile are staged in smem with cp.async
   const int* status;  // abort when status[0] != 0 (failed factorisation)
   const int* csr_off;
   const int* slot_flow;
@@ -107,11 +108,12 @@ __host__ __device__ inline int pass_ntiles(int mpad) {
 }
 
 struct PassSmem {
-  size_t U, parts, dcs, dns, qc, qn, ebuf, ethb, red, emap, sflow, sl, sb, total;
+  size_t fbuf, U, parts, dcs, dns, qc, qn, ebuf, ethb, red, emap, sflow, sl, sb, total;
 };
-__host__ __device__ inline PassSmem pass_smem_layout(int kmax, bool calib) {
+__host__ __device__ inline PassSmem pass_smem_layout(int kmax, bool calib, bool stage) {
   PassSmem s;
   size_t o = 0;
+  s.fbuf = o; o += stage ? sizeof(float4) * (size_t)kmax * kSub : 0;
   const int nparts = calib ? 6 : 3;  // phase A: C, gd, acc ; phase B: C, gd (+ E_theta x4)
   s.ethb = o; o += calib ? sizeof(double) * kPassWarps * kEdgeSlots * 32 : 0;
   s.red = o; o += sizeof(double) * kPassWarps * 16;
@@ -168,7 +170,8 @@ __global__ void __launch_bounds__(kPassThreads, 1) pass_kernel(const PassArgs A)
   if (A.status != nullptr && A.status[0] != 0) return;
   extern __shared__ __align__(16) unsigned char smem[];
   constexpr int NVE = kEdgeVals + (CALIB ? kCalibVals : 0);
-  const PassSmem L = pass_smem_layout(A.kmax, CALIB);
+  const PassSmem L = pass_smem_layout(A.kmax, CALIB, A.stage != 0);
+  float4* fbuf = reinterpret_cast<float4*>(smem + L.fbuf);  // [k][kSub] flow records
   float* U = reinterpret_cast<float*>(smem + L.U);
   float* Mg = reinterpret_cast<float*>(smem + L.U);  // segment end only: [32][kPassThreads]
   float* parts = reinterpret_cast<float*>(smem + L.parts);
@@ -269,11 +272,33 @@ __global__ void __launch_bounds__(kPassThreads, 1) pass_kernel(const PassArgs A)
       kappa = (gs[1] - hd) / gs[0];
     }
 
+    // cp.async staging of a sub-tile's flow records (16 B each) and disparities;
+    // out-of-range pixels are zero-filled
+    auto prefetch = [&](int tile) {
+      const int pb = tile * kSub;
+      for (int x = tid; x < k * kSub; x += kPassThreads) {
+        const int a = x >> 8, pl = x & (kSub - 1), p = pb + pl;
+        const float4* src = A.flow + (size_t)sflow[a] * P + (p < P ? p : 0);
+        const unsigned dst = (unsigned)__cvta_generic_to_shared(fbuf + x);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
+                     "r"(p < P ? 16 : 0));
+      }
+      if (tid < kSub) {
+        const int p = pb + tid;
+        const float* src = A.d_cur + (size_t)f * P + (p < P ? p : 0);
+        const unsigned dst = (unsigned)__cvta_generic_to_shared(dcs + tid);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst), "l"(src), "r"(p < P ? 4 : 0));
+      }
+      asm volatile("cp.async.commit_group;");
+    };
+    if (A.stage) prefetch(A.seg_t0[sg]);
+
     for (int tile = A.seg_t0[sg]; tile < A.seg_t1[sg]; ++tile) {
       const int pbase = tile * kSub;
+      if (A.stage) asm volatile("cp.async.wait_all;" ::: "memory");
       if (tid < kSub) {
         const int p = pbase + tid;
-        dcs[tid] = p < P ? A.d_cur[(size_t)f * P + p] : 1.f;
+        if (!A.stage) dcs[tid] = p < P ? A.d_cur[(size_t)f * P + p] : 0.f;
         const float pu = (float)(p % A.W), pv = (float)(p / A.W);
         qcs[tid] = make_float2((pu - cxc) / fxc, (pv - cyc) / fyc);
         qns[tid] = make_float2((pu - cxn) / fxn, (pv - cyn) / fyn);
@@ -290,7 +315,8 @@ __global__ void __launch_bounds__(kPassThreads, 1) pass_kernel(const PassArgs A)
           for (int i = 0; i < 2; ++i) {
             const int pl = sl0 + lane + 32 * i, p = pbase + pl;
             const bool in = p < P;
-            const float4 fw = in ? __ldg(fl4 + p) : make_float4(0.f, 0.f, 0.f, 0.f);
+            const float4 fw = A.stage ? fbuf[a * kSub + pl]
+                                      : (in ? __ldg(fl4 + p) : make_float4(0.f, 0.f, 0.f, 0.f));
             const float dc = dcs[pl];
             const float2 q = qcs[pl];
             const float qx = q.x, qy = q.y;
@@ -369,7 +395,8 @@ __global__ void __launch_bounds__(kPassThreads, 1) pass_kernel(const PassArgs A)
         for (int i = 0; i < 2; ++i) {
           const int pl = sl0 + lane + 32 * i, p = pbase + pl;
           const bool in = p < P;
-          const float4 fw = in ? __ldg(fl4 + p) : make_float4(0.f, 0.f, 0.f, 0.f);
+          const float4 fw = A.stage ? fbuf[a * kSub + pl]
+                                    : (in ? __ldg(fl4 + p) : make_float4(0.f, 0.f, 0.f, 0.f));
           const float dn = dns[pl];
           const float2 q = qns[pl];
           const float qx = q.x, qy = q.y;
@@ -461,6 +488,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) pass_kernel(const PassArgs A)
         }
       }
       __syncthreads();
+      if (A.stage && tile + 1 < A.seg_t1[sg]) prefetch(tile + 1);  // overlaps the GEMM
       // ------------------------------------------------------------ per pixel
       if (tid < kSub) {
         const int p = pbase + tid;
