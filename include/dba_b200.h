@@ -134,6 +134,7 @@ typedef struct {
   int32_t max_out_degree;
   int32_t n_split;          /* pixel splits per frame in the fused pass */
   int32_t gauge_frame;      /* -1 when the scale gauge is off */
+  int32_t solve_ctas;       /* 1: one factorisation chain, 2: top/bottom chains */
   int64_t workspace_bytes;
 } dba_plan_info;
 

@@ -70,7 +70,7 @@ class PlanInfo(ctypes.Structure):
     _fields_ = [
         ("n_reduced", c_i32), ("n_free_poses", c_i32), ("band_blocks", c_i32),
         ("frame_begin", c_i32), ("frame_end", c_i32), ("n_local_edges", c_i32),
-        ("max_out_degree", c_i32), ("n_split", c_i32), ("gauge_frame", c_i32),
+        ("max_out_degree", c_i32), ("n_split", c_i32), ("gauge_frame", c_i32), ("solve_ctas", c_i32),
         ("workspace_bytes", ctypes.c_int64),
     ]
 

@@ -75,7 +75,7 @@ struct Layout {
   size_t off_F, off_f, units, contrib, meta_end;
   // state
   size_t poses[2], intr[2], disps[2], xi, delta, lin, back, adj;
-  size_t part_edge, part_M, part_w, part_frame, Fbuf, sys[2], gstate[2], Lband, flags, gauge, total;
+  size_t part_edge, part_M, part_w, part_frame, Fbuf, sys[2], gstate[2], Lband, rLband, mid, flags, gauge, total;
 };
 
 }  // namespace
@@ -87,7 +87,8 @@ struct dba_plan {
   int n_tiles = 0, G = 0, nseg = 0, n_units = 0, nve = kEdgeVals, stage = 1;
   size_t pass_smem = 0, solve_smem = 0;
   long long sys_len = 0;  // doubles in one packed reduced system
-  long long band_len = 0, theta_off = 0, thth_off = 0, y_off = 0, energy_off = 0;
+  long long band_len = 0, rband_off = 0, theta_off = 0, thth_off = 0, y_off = 0, energy_off = 0;
+  int two_sided = 0, m_top = 0;  // two-CTA solve: pivots of the top chain
   std::vector<int> fixed_ridx;
   std::vector<int> local_edges;  // input edge id of each local flow row
   Layout L{};
@@ -279,7 +280,12 @@ int dba_plan_create(const dba_problem_desc* d, dba_plan** out) {
   p->BW = (p->nb > 0) ? std::min(BW, p->nb - 1) : 0;
   const int W1 = p->BW + 1;
   p->band_len = (long long)p->nb * W1 * 36;
-  p->theta_off = p->band_len;
+  // long chains are factored from both ends at once (solve2_kernel); the gather
+  // then also writes the band in reversed block order for the bottom chain
+  p->two_sided = (p->BW >= 1 && p->nb >= 4 * p->BW + 16) ? 1 : 0;
+  p->m_top = p->two_sided ? (p->nb - p->BW) / 2 : 0;
+  p->rband_off = p->band_len;
+  p->theta_off = p->band_len * (p->two_sided ? 2 : 1);
   p->thth_off = p->theta_off + (long long)p->nb * 24;
   p->y_off = p->thth_off + 16;
   p->energy_off = p->y_off + p->n_red;
@@ -416,6 +422,26 @@ int dba_plan_create(const dba_problem_desc* d, dba_plan** out) {
         u.c1 = (int)contrib.size();
         units.push_back(u);
       }
+    if (p->two_sided) {
+      // reversed order: block (a', c') of the flipped system is block
+      // (nb-1-c', nb-1-a') transposed, at the same band position
+      for (int ar = 0; ar < p->nb; ++ar)
+        for (int pos = 0; pos < W1; ++pos) {
+          const int cr = ar - p->BW + pos;
+          GatherUnit u;
+          u.dst = p->rband_off + ((long long)ar * W1 + pos) * 36;
+          u.rows = 6;
+          u.cols = 6;
+          u.trans = 1;
+          u.c0 = u.c1 = 0;
+          if (cr >= 0) {
+            const GatherUnit& src = units[(size_t)(p->nb - 1 - cr) * W1 + pos];
+            u.c0 = src.c0;
+            u.c1 = src.c1;
+          }
+          units.push_back(u);
+        }
+    }
     if (p->calib) {
       for (int c = 0; c < p->nb; ++c) {
         GatherUnit u;
@@ -527,6 +553,8 @@ int dba_plan_create(const dba_problem_desc* d, dba_plan** out) {
   L.part_frame = take(sizeof(double) * kFrameVals * (size_t)p->nseg);
   L.Fbuf = take(sizeof(double) * nF);
   L.Lband = take(sizeof(double) * std::max<long long>(p->band_len, 1));
+  L.rLband = take(sizeof(double) * (p->two_sided ? p->band_len : 1));
+  L.mid = take(sizeof(double) * (p->two_sided ? solve_mid_len(p->BW) : 1));
   L.flags = take(sizeof(Readback));
   L.gauge = take(sizeof(double) * 4);
   L.total = o;
@@ -574,6 +602,7 @@ int dba_plan_get_info(const dba_plan* p, dba_plan_info* info) {
   info->max_out_degree = p->kmax;
   info->n_split = p->G;
   info->gauge_frame = p->gauge_frame;
+  info->solve_ctas = p->two_sided ? 2 : 1;
   info->workspace_bytes = (int64_t)p->L.total;
   return DBA_OK;
 }
@@ -827,10 +856,18 @@ int launch_solve(Ctx& c, int slot, double lam) {
   a.theta = s + p->theta_off;
   a.thth = s + p->thth_off;
   a.y = s + p->y_off;
+  a.rband = s + p->rband_off;
   a.Lband = c.at<double>(p->L.Lband);
+  a.rLband = c.at<double>(p->L.rLband);
+  a.mid = c.at<double>(p->L.mid);
   a.delta = c.at<double>(p->L.delta);
   a.cond = &c.at<Readback>(p->L.flags)->cond;
-  auto kern = (p->BW <= 5) ? solve_kernel<1> : (p->BW <= 10) ? solve_kernel<2> : solve_kernel<5>;
+  a.m_top = p->m_top;
+  void (*kern)(const SolveArgs);
+  if (p->two_sided)
+    kern = (p->BW <= 5) ? solve2_kernel<1> : (p->BW <= 10) ? solve2_kernel<2> : solve2_kernel<5>;
+  else
+    kern = (p->BW <= 5) ? solve_kernel<1> : (p->BW <= 10) ? solve_kernel<2> : solve_kernel<5>;
   DBA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->solve_smem));
   auto& pr = p->prof;
   std::pair<int, int> ev{-1, -1};
@@ -838,7 +875,12 @@ int launch_solve(Ctx& c, int slot, double lam) {
     if (int s2 = ev_pair(c, ev)) return s2;
     DBA_CUDA(cudaEventRecord(pr.pool[ev.first], c.st));
   }
-  kern<<<1, kSolveThreads, p->solve_smem, c.st>>>(a);
+  if (p->two_sided) {
+    void* args[] = {&a};
+    DBA_CUDA(cudaLaunchCooperativeKernel((const void*)kern, dim3(2), dim3(kSolveThreads), args, p->solve_smem, c.st));
+  } else {
+    kern<<<1, kSolveThreads, p->solve_smem, c.st>>>(a);
+  }
   pr.launches++;
   pr.solve_launches++;
   if (pr.on) {

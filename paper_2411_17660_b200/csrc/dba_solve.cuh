@@ -4,26 +4,31 @@
 // frame couples the poses {i} U out(i), so with the (free-pose) ordering used
 // by the plan every nonzero 6x6 block (a, c) satisfies |a - c| <= BW.  The
 // intrinsics (4 rows, "global block") form a dense border that is
-// eliminated last.  One CTA factors the band as a block LDL^T,
+// eliminated last.  The band is factored as a block LDL^T,
 //     L_ab = S_ab D_b^-1,   S_ac -= L_ab S_cb^T,   D_b = S_bb (updated),
 // with a sliding window of BW+1 block rows resident in shared memory.  D_b is
 // SPD iff the damped system is; D_b^-1 comes from two 3x3 adjugate inverses
-// (leading-minor test = the Cholesky pivot test), which keeps only two
-// reciprocals on the pivot chain instead of six square roots.
+// (leading-minor test = the Cholesky pivot test).  Damping lambda is added to a
+// diagonal block when it becomes a pivot.
 //
-// Latency engineering (the factorisation is a chain of nb dependent pivots):
-//  * one critical warp (warp 7: the arbiter issues higher warp ids first, and
-//    warp 3 that shares its scheduler only issues cp.async) forms the NEXT
-//    pivot — L_{b+1,b}, D_{b+1}, D_{b+1}^-1 — with all 32 lanes, while 6 warps
-//    apply step b's trailing update: one CTA barrier per step;
-//  * rows entering the window are copied global->shared with cp.async a step
-//    ahead (the damping of their diagonal block is added when it becomes a pivot);
+// The factorisation is a chain of dependent 6x6 pivots, so:
+//  * two-sided (solve2_kernel, cooperative, 2 CTAs): CTA 0 eliminates poses
+//    0..m-1 top-down while CTA 1 eliminates nb-1..m+BW bottom-up on the reversed
+//    band (written by gather); the BW-block middle receives both Schur updates,
+//    is combined (T + B - S) and solved densely, then both halves back-substitute
+//    in parallel — half the chain length of the one-sided solve_kernel;
+//  * inside a chain one critical warp (warp 7: the arbiter issues higher warp ids
+//    first, and warp 3 on its scheduler only issues cp.async) forms the NEXT
+//    pivot while 6 warps apply the trailing update: one CTA barrier per step;
+//  * rows entering the window are copied with cp.async a step ahead;
 //  * back-substitution: w_b = D_b^-1 z_b for all b in parallel, then one warp
-//    sweeps b = nb-1..0 without CTA barriers, folding x_b = w_b - sum L_ab^T x_a
-//    into the BW blocks above it with the next factor row prefetched from L2.
+//    sweeps without CTA barriers, folding x_b = w_b - sum L_ab^T x_a into the BW
+//    blocks above, factor rows streaming through an 8-deep cp.async ring.
 // A non-SPD pivot aborts with status 1 (the host raises lambda).
 // The Cholesky pivots of the intrinsics Schur block give the A9 estimate.
 #pragma once
+
+#include <cooperative_groups.h>
 
 #include "dba_common.cuh"
 
@@ -35,46 +40,43 @@ constexpr int kStageWarp = 3;       // shares the critical warp's scheduler; onl
 constexpr int kTrailThreads = 192;  // warps 0,1,2,4,5,6
 constexpr int kMaxBand = 24;        // compiled limit on BW
 
-#ifdef DBA_SOLVE_PROF
-// clock64() phase accounting for the microbenchmark in scratch/ (not in the library build)
-#define SPROF(k)                                              \
-  do {                                                        \
-    prof_sink += *(volatile int*)&fail;                       \
-    const long long _t = clock64();                           \
-    if (lane == 0 && (warp == kCritWarp || warp == 0 || warp == 3)) \
-      prof_acc[k] += _t - prof_t;                             \
-    prof_t = _t;                                              \
-  } while (0)
-__device__ long long g_prof[64];
-#else
-#define SPROF(k) \
-  do {           \
-  } while (0)
-#endif
-
 struct SolveArgs {
   int nb, BW, calib;
   double lambda;
   int* status;
   const double* band;   // nb*(BW+1)*36, block (a,c) at (a*(BW+1) + c-a+BW)*36
+  const double* rband;  // the same band in reversed block order (two-sided solve)
   const double* theta;  // nb*24 (4x6 per block)
   const double* thth;   // 16
   const double* y;      // 6 nb + 4 calib
-  double* Lband;        // factor rows: L_ab at (a, c=b); slot BW holds D_a^-1
+  double* Lband;        // factor rows (top / single chain): L_ab at (a, c=b); slot BW = D_a^-1
+  double* rLband;       // factor rows of the bottom chain (reversed indexing)
+  double* mid;          // two-sided exchange scratch (see solve_mid_len)
   double* delta;        // 6 nb + 4 calib
   double* cond;         // theta pivot ratio
+  int m_top;            // two-sided: pivots of the top chain (0: one-sided)
 };
 
+// doubles of the two-sided exchange scratch
+__host__ __device__ inline long long solve_mid_len(int BW) {
+  const long long per = (long long)BW * BW * 36 + 6 * BW + (long long)BW * 24 + 16 + 4;
+  return 2 * per + (long long)BW * BW * 36 /* middle factor rows */ + 6 * BW + 4 /* solution */;
+}
+
 struct SolveSmem {
-  size_t win, th, thL, z, dinv, pbuf, cbuf, tbuf, pairs, total;
+  size_t win, th, thL, z, thm, thLm, zm, dinv, pbuf, cbuf, tbuf, pairs, total;
 };
 __host__ __device__ inline SolveSmem solve_smem_layout(int nb, int BW, int calib) {
   SolveSmem s;
   size_t o = 0;
-  s.win = o; o += sizeof(double) * (size_t)(BW + 1) * (BW + 1) * 36;
+  // the window is reused by the backward sweep as an 8-row cp.async ring
+  s.win = o; o += sizeof(double) * (size_t)((BW + 1) > 8 ? (BW + 1) : 8) * (BW + 1) * 36;
   s.th = o; o += sizeof(double) * (calib ? (size_t)nb * 24 + 16 : 0);
   s.thL = o; o += sizeof(double) * (calib ? (size_t)nb * 24 : 0);
   s.z = o; o += sizeof(double) * ((size_t)6 * nb + 4);
+  s.thm = o; o += sizeof(double) * (calib ? (size_t)BW * 24 + 16 : 0);
+  s.thLm = o; o += sizeof(double) * (calib ? (size_t)BW * 24 : 0);
+  s.zm = o; o += sizeof(double) * ((size_t)6 * BW + 4);
   s.dinv = o; o += sizeof(double) * 2 * 36;
   s.pbuf = o; o += sizeof(double) * (size_t)(BW + 1) * 36;
   s.cbuf = o; o += sizeof(double) * 2 * 36;
@@ -105,17 +107,17 @@ __device__ __forceinline__ bool inv3_spd(const double m[9], double o[9]) {
   return ok;
 }
 
-// inverse of a 6x6 SPD block via [A B; B^T C]:  A^-1, T = A^-1 B, C' = C - B^T T,
-// D^-1 = [A^-1 + T C'^-1 T^T, -T C'^-1; -C'^-1 T^T, C'^-1].  false if not SPD.
-__device__ __forceinline__ bool inv6_spd(const double* D, double* Di) {
+// inverse of a 6x6 SPD block (+ lam I) via [A B; B^T C]:  A^-1, T = A^-1 B,
+// C' = C - B^T T, D^-1 = [A^-1 + T C'^-1 T^T, -T C'^-1; -C'^-1 T^T, C'^-1].
+__device__ __forceinline__ bool inv6_spd(const double* D, double lam, double* Di) {
   double A[9], B[9], C[9], Ai[9], T[9], Cs[9], Ci[9], U[9];
 #pragma unroll
   for (int r = 0; r < 3; ++r)
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-      A[3 * r + c] = 0.5 * (D[6 * r + c] + D[6 * c + r]);
+      A[3 * r + c] = 0.5 * (D[6 * r + c] + D[6 * c + r]) + (r == c ? lam : 0.0);
       B[3 * r + c] = D[6 * r + c + 3];
-      C[3 * r + c] = 0.5 * (D[6 * (r + 3) + c + 3] + D[6 * (c + 3) + r + 3]);
+      C[3 * r + c] = 0.5 * (D[6 * (r + 3) + c + 3] + D[6 * (c + 3) + r + 3]) + (r == c ? lam : 0.0);
     }
   bool ok = inv3_spd(A, Ai);
 #pragma unroll
@@ -169,132 +171,112 @@ __device__ __forceinline__ void row_times(const double* v, const double* Di, dou
   }
 }
 
-template <int NS>  // backward-sweep prefetch slots per lane: ceil(6 BW / 32)
-__global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const SolveArgs A) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  const SolveSmem Ls = solve_smem_layout(A.nb, A.BW, A.calib);
-  double* win = reinterpret_cast<double*>(smem + Ls.win);
-  double* th = reinterpret_cast<double*>(smem + Ls.th);
-  double* thL = reinterpret_cast<double*>(smem + Ls.thL);
-  double* z = reinterpret_cast<double*>(smem + Ls.z);
-  double* dinv = reinterpret_cast<double*>(smem + Ls.dinv);
-  double* pbuf = reinterpret_cast<double*>(smem + Ls.pbuf);
-  double* cbuf = reinterpret_cast<double*>(smem + Ls.cbuf);
-  double* tbuf = reinterpret_cast<double*>(smem + Ls.tbuf);
-  short2* pairs = reinterpret_cast<short2*>(smem + Ls.pairs);
-  __shared__ int fail;
+// shared-memory working set of one elimination chain
+struct ChainSm {
+  double* win;   // (BW+1) window rows x (BW+1) blocks x 36
+  double* th;    // theta border: ncols x 24, then theta-theta (16)
+  double* thL;   // L_tb per eliminated pivot (ncols x 24)
+  double* z;     // rhs: 6 ncols, then theta (4)
+  double* dinv;  // D_b^-1 double buffer
+  double* pbuf;  // panels of the current step
+  double* cbuf;  // critical-warp scratch
+  double* tbuf;  // theta panel
+  short2* pairs;
+  int* fail;
+};
+
+// Forward block-LDL^T over pivots [0, npiv) of a band whose rows [0, nrows) live in
+// `band` (local orientation).  The window must hold rows 0..min(BW, nrows-1) on
+// entry.  Rows npiv..nrows-1 receive the Schur updates but are not pivoted (their
+// diagonal block includes the critical warp's update).  ncols: offset of the theta
+// rows in th / z.  Writes factor rows [0, nrows) to Lband (off-diagonal L blocks) and
+// D_b^-1 to the diagonal slot of rows [0, npiv).
+__device__ inline void chain_forward(const ChainSm& S, const double* band, double* Lband, int nrows, int npiv,
+                                     int BW, int calib, int ncols, double lam) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int nb = A.nb, BW = A.BW, W1 = BW + 1, NR = W1 * 36;
-  const double lam = A.lambda;
-  const int nz = 6 * nb + (A.calib ? 4 : 0);
+  const int W1 = BW + 1, NR = W1 * 36;
   const bool crit = warp == kCritWarp;
   const bool trail = (warp & 3) != 3;
-  const int gt = (warp - (warp >> 2)) * 32 + lane;  // index within the trailing group
-  if (tid == 0) fail = 0;
-#ifdef DBA_SOLVE_PROF
-  long long prof_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  long long prof_t = clock64();
-  int prof_sink = 0;
-#endif
-
-  // ---- load: rows 0..min(BW, nb-1), theta border, rhs, pair table
-  const int r0 = min(BW, nb - 1);
-  for (int x = tid; x < (r0 + 1) * NR; x += kSolveThreads) {
-    const int rem = x % NR, pos = rem / 36, e = rem % 36;
-    double v = A.band[x];
-    if (pos == BW && (e / 6) == (e % 6)) v += lam;
-    win[x] = v;  // slot(a) = a for a <= BW
-  }
-  if (A.calib) {
-    for (int x = tid; x < nb * 24; x += kSolveThreads) th[x] = A.theta[x];
-    if (tid < 16) th[nb * 24 + tid] = A.thth[tid] + ((tid / 4 == tid % 4) ? lam : 0.0);
-  }
-  for (int x = tid; x < nz; x += kSolveThreads) z[x] = A.y[x];
+  const int gt = (warp - (warp >> 2)) * 32 + lane;
   if (tid == 0) {
     int q = 0;
     for (int ao = 0; ao < BW; ++ao)
-      for (int pi = 0; pi <= ao; ++pi) pairs[q++] = make_short2((short)ao, (short)pi);
+      for (int pi = 0; pi <= ao; ++pi) S.pairs[q++] = make_short2((short)ao, (short)pi);
   }
-  __syncthreads();
-  if (nb > 0 && crit && lane == 0) {
+  if (npiv > 0 && crit && lane == 0) {
     double Di[36];
-    if (!inv6_spd(win + (size_t)BW * 36, Di)) fail = 1;  // block (0,0)
-    for (int x = 0; x < 36; ++x) dinv[x] = Di[x];
+    if (!inv6_spd(S.win + (size_t)BW * 36, lam, Di)) *S.fail = 1;  // block (0,0)
+    for (int x = 0; x < 36; ++x) S.dinv[x] = Di[x];
   }
-  // rows entering the window: warp 3 issues cp.async for row b+BW+1 during step b
-  auto row_stage = [&](int a, int slot) {
-    if (warp != kStageWarp || a >= nb) return;
-    const char* src = reinterpret_cast<const char*>(A.band + (size_t)a * NR);
-    const unsigned dst = (unsigned)__cvta_generic_to_shared(win + (size_t)slot * NR);
-    for (int q = lane; q < NR / 2; q += 32)
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + 16 * q), "l"(src + 16 * q));
-    asm volatile("cp.async.commit_group;");
-  };
   __syncthreads();
-
   int sb = 0;  // slot of block row b (= b % W1)
-  for (int b = 0; b < nb && !fail; ++b) {
-    const int amax = min(nb - 1, b + BW);
+  for (int b = 0; b < npiv && !*S.fail; ++b) {
+    const int amax = min(nrows - 1, b + BW);
     const int na = amax - b;
-    const double* Db = dinv + 36 * (b & 1);  // D_b^-1
+    const double* Db = S.dinv + 36 * (b & 1);  // D_b^-1
     auto wb = [&](int a, int c) -> double* {
       int sl = sb + (a - b);
       sl = sl >= W1 ? sl - W1 : sl;
-      return win + ((size_t)sl * W1 + (c - a + BW)) * 36;
+      return S.win + ((size_t)sl * W1 + (c - a + BW)) * 36;
     };
-    const double* zb = z + 6 * b;
-    SPROF(0);
+    const double* zb = S.z + 6 * b;
     if (crit) {
-      // ---- next pivot: L_{b+1,b} = S_{b+1,b} D_b^-1, D_{b+1} = S_{b+1,b+1} - L S^T, D_{b+1}^-1
+      // next pivot: L_{b+1,b} = S_{b+1,b} D_b^-1, S_{b+1,b+1} -= L S^T, D_{b+1}^-1
       if (na > 0) {
         const double* S1 = wb(b + 1, b);
-        const double* S11 = wb(b + 1, b + 1);
-        for (int e = lane; e < 36; e += 32) {
-          const int r = e / 6, c = e % 6;
-          double s = 0.0;
+        double* S11 = wb(b + 1, b + 1);
+        double* Lr = S.cbuf;
+        const int e0 = lane, e1 = lane + 32;
+        const bool h1 = e1 < 36;
+        const int r0 = e0 / 6, c0 = e0 % 6, r1 = h1 ? e1 / 6 : 0, c1 = h1 ? e1 % 6 : 0;
+        {
+          double s0 = 0.0, s1 = 0.0;
 #pragma unroll
-          for (int k = 0; k < 6; ++k) s = fma(S1[6 * r + k], Db[6 * k + c], s);
-          cbuf[e] = s;  // L_{b+1,b}
+          for (int k = 0; k < 6; ++k) {
+            s0 = fma(S1[6 * r0 + k], Db[6 * k + c0], s0);
+            s1 = fma(S1[6 * r1 + k], Db[6 * k + c1], s1);
+          }
+          Lr[e0] = s0;
+          if (h1) Lr[e1] = s1;
         }
         __syncwarp();
-        SPROF(1);
-        double* Dn = cbuf + 36;
-        const double dl = (b + 1 > BW) ? lam : 0.0;  // rows staged by cp.async carry no damping
-        for (int e = lane; e < 36; e += 32) {
-          const int r = e / 6, c = e % 6;
-          double s = S11[e] + ((r == c) ? dl : 0.0);
+        {
+          double d0 = S11[e0], d1 = h1 ? S11[e1] : 0.0;
 #pragma unroll
-          for (int k = 0; k < 6; ++k) s = fma(-cbuf[6 * r + k], S1[6 * c + k], s);
-          Dn[e] = s;
-        }
-        if (lane < 6) {
-          double s = z[6 * (b + 1) + lane];
+          for (int k = 0; k < 6; ++k) {
+            d0 = fma(-Lr[6 * r0 + k], S1[6 * c0 + k], d0);
+            d1 = fma(-Lr[6 * r1 + k], S1[6 * c1 + k], d1);
+          }
+          if (lane < 6) {
+            double s = S.z[6 * (b + 1) + lane];
 #pragma unroll
-          for (int k = 0; k < 6; ++k) s = fma(-cbuf[6 * lane + k], zb[k], s);
-          z[6 * (b + 1) + lane] = s;
+            for (int k = 0; k < 6; ++k) s = fma(-Lr[6 * lane + k], zb[k], s);
+            S.z[6 * (b + 1) + lane] = s;
+          }
+          __syncwarp();
+          S11[e0] = d0;  // keep the updated block (non-pivot rows are exported from here)
+          if (h1) S11[e1] = d1;
         }
         __syncwarp();
-        SPROF(2);
-        if (lane == 0) {
+        if (lane == 0 && b + 1 < npiv) {
           double Di[36];
-          if (!inv6_spd(Dn, Di)) fail = 1;
-          double* Dnx = dinv + 36 * ((b + 1) & 1);
+          if (!inv6_spd(S11, lam, Di)) *S.fail = 1;
+          double* Dnx = S.dinv + 36 * ((b + 1) & 1);
 #pragma unroll
           for (int x = 0; x < 36; ++x) Dnx[x] = Di[x];
         }
       }
-      SPROF(3);
-      for (int e = lane; e < 36; e += 32) A.Lband[((size_t)b * W1 + BW) * 36 + e] = Db[e];
+      for (int e = lane; e < 36; e += 32) Lband[((size_t)b * W1 + BW) * 36 + e] = Db[e];
     } else if (trail) {
-      // ---- panels L_ab = S_ab D_b^-1 (a in (b, amax]), L_tb = S_tb D_b^-1
-      const int prow = 6 * na + (A.calib ? 4 : 0);
+      // panels L_ab = S_ab D_b^-1 (a in (b, amax]), L_tb = S_tb D_b^-1
+      const int prow = 6 * na + (calib ? 4 : 0);
       for (int x = gt; x < prow; x += kTrailThreads) {
         if (x < 6 * na) {
           const int ao = x / 6, r = x % 6;
           double o[6];
           row_times(wb(b + 1 + ao, b) + 6 * r, Db, o);
-          double* pb = pbuf + 36 * ao + 6 * r;
-          double* lb = A.Lband + ((size_t)(b + 1 + ao) * W1 + (BW - 1 - ao)) * 36 + 6 * r;
+          double* pb = S.pbuf + 36 * ao + 6 * r;
+          double* lb = Lband + ((size_t)(b + 1 + ao) * W1 + (BW - 1 - ao)) * 36 + 6 * r;
 #pragma unroll
           for (int c = 0; c < 6; ++c) {
             pb[c] = o[c];
@@ -302,26 +284,24 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const SolveArgs
           }
         } else {
           const int tt = x - 6 * na;
-          row_times(th + (size_t)b * 24 + 6 * tt, Db, tbuf + 6 * tt);
+          row_times(S.th + (size_t)b * 24 + 6 * tt, Db, S.tbuf + 6 * tt);
         }
       }
-      SPROF(1);
       asm volatile("bar.sync 1, %0;" ::"n"(kTrailThreads) : "memory");
-      SPROF(2);
-      // ---- trailing update S_ac -= L_ab S_cb^T (except (b+1,b+1)), border, rhs
+      // trailing update S_ac -= L_ab S_cb^T (except (b+1,b+1)), border, rhs
       const int npair = na * (na + 1) / 2;
       const int n1 = npair * 3;
-      const int n2 = A.calib ? na * 4 : 0;
-      const int n3 = A.calib ? 4 : 0;
-      const int n4 = 6 * (na > 0 ? na - 1 : 0) + (A.calib ? 4 : 0);
+      const int n2 = calib ? na * 4 : 0;
+      const int n3 = calib ? 4 : 0;
+      const int n4 = 6 * (na > 0 ? na - 1 : 0) + (calib ? 4 : 0);
       const int ntot = n1 + n2 + n3 + n4;
       for (int x = gt; x < ntot; x += kTrailThreads) {
         if (x < n1) {
           const int pidx = x / 3, rr = 2 * (x % 3);
           if (pidx == 0) continue;  // (b+1, b+1): critical warp
-          const short2 pr = pairs[pidx];
+          const short2 pr = S.pairs[pidx];
           const int a = b + 1 + pr.x, cc = b + 1 + pr.y;
-          const double* La = pbuf + 36 * pr.x + 6 * rr;
+          const double* La = S.pbuf + 36 * pr.x + 6 * rr;
           const double2* Sc = reinterpret_cast<const double2*>(wb(cc, b));
           double2* O = reinterpret_cast<double2*>(wb(a, cc) + 6 * rr);
           double ar[2][6], o[2][6];
@@ -355,9 +335,9 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const SolveArgs
         } else if (x < n1 + n2) {
           const int y2 = x - n1, co = y2 / 4, tt = y2 % 4;
           const int cc = b + 1 + co;
-          const double* Lt = tbuf + 6 * tt;
+          const double* Lt = S.tbuf + 6 * tt;
           const double* Sc = wb(cc, b);
-          double* O = th + (size_t)cc * 24 + 6 * tt;
+          double* O = S.th + (size_t)cc * 24 + 6 * tt;
 #pragma unroll
           for (int c = 0; c < 6; ++c) {
             double s = O[c];
@@ -367,11 +347,11 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const SolveArgs
           }
         } else if (x < n1 + n2 + n3) {
           const int tt = x - n1 - n2;
-          const double* Lt = tbuf + 6 * tt;
-          double* O = th + (size_t)nb * 24 + 4 * tt;
+          const double* Lt = S.tbuf + 6 * tt;
+          double* O = S.th + (size_t)ncols * 24 + 4 * tt;
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
-            const double* Su = th + (size_t)b * 24 + 6 * u;
+            const double* Su = S.th + (size_t)b * 24 + 6 * u;
             double s = O[u];
 #pragma unroll
             for (int d = 0; d < 6; ++d) s = fma(-Lt[d], Su[d], s);
@@ -382,12 +362,12 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const SolveArgs
           const double* Lr;
           double* zt;
           if (q < 6 * (na - 1)) {
-            Lr = pbuf + 36 + 6 * q;  // rows a >= b+2
-            zt = z + 6 * (b + 2) + q;
+            Lr = S.pbuf + 36 + 6 * q;  // rows a >= b+2
+            zt = S.z + 6 * (b + 2) + q;
           } else {
             const int tt = q - 6 * (na > 0 ? na - 1 : 0);
-            Lr = tbuf + 6 * tt;
-            zt = z + 6 * nb + tt;
+            Lr = S.tbuf + 6 * tt;
+            zt = S.z + 6 * ncols + tt;
           }
           double s = *zt;
 #pragma unroll
@@ -395,129 +375,294 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const SolveArgs
           *zt = s;
         }
       }
-      if (A.calib && gt < 24) thL[(size_t)b * 24 + gt] = tbuf[gt];  // L_tb for the backward sweep
-    } else {
-      // ---- warp 3: copy row b+BW+1 into row b's slot (free during step b)
-      if (b + BW + 1 < nb) {
-        row_stage(b + BW + 1, sb);
-        asm volatile("cp.async.wait_all;" ::: "memory");
-      }
+      if (calib && gt < 24) S.thL[(size_t)b * 24 + gt] = S.tbuf[gt];  // L_tb for the backward sweep
+    } else if (warp == kStageWarp && band != nullptr && b + BW + 1 < nrows) {
+      // copy row b+BW+1 into row b's slot (free during step b)
+      const char* src = reinterpret_cast<const char*>(band + (size_t)(b + BW + 1) * NR);
+      const unsigned dst = (unsigned)__cvta_generic_to_shared(S.win + (size_t)sb * NR);
+      for (int q = lane; q < NR / 2; q += 32)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + 16 * q), "l"(src + 16 * q));
+      asm volatile("cp.async.commit_group;");
+      asm volatile("cp.async.wait_all;" ::: "memory");
     }
-    SPROF(4);
     __syncthreads();
-    SPROF(5);
     sb = (sb + 1 == W1) ? 0 : sb + 1;
   }
-  if (fail) {
-    if (tid == 0) A.status[0] = 1;
-    return;
-  }
-  // ---- theta block: Cholesky pivots (A9), solve
-  if (A.calib && tid == 0) {
-    double* T = th + (size_t)nb * 24;
-    double L[16];
-    bool ok = true;
-    double pmax = 0.0, pmin = 1e300;
-    for (int x = 0; x < 16; ++x) L[x] = 0.0;
-    for (int c = 0; c < 4; ++c) {
-      double s = T[4 * c + c];
-      for (int d = 0; d < c; ++d) s -= L[4 * c + d] * L[4 * c + d];
-      if (!(s > 0.0) || !isfinite(s)) ok = false;
-      pmax = fmax(pmax, s);
-      pmin = fmin(pmin, s);
-      const double l = sqrt(fmax(s, 1e-300));
-      L[4 * c + c] = l;
-      for (int r = c + 1; r < 4; ++r) {
-        double t = T[4 * r + c];
-        for (int d = 0; d < c; ++d) t -= L[4 * r + d] * L[4 * c + d];
-        L[4 * r + c] = t / l;
-      }
+}
+
+// theta block (4x4 Schur complement + lam): Cholesky, forward+backward solve in
+// place of zt, A9 condition estimate.  Single thread.
+__device__ inline bool theta_solve(const double* T, double* zt, double lam, double* cond) {
+  double L[16];
+  bool ok = true;
+  double pmax = 0.0, pmin = 1e300;
+  for (int x = 0; x < 16; ++x) L[x] = 0.0;
+  for (int c = 0; c < 4; ++c) {
+    double s = T[4 * c + c] + lam;
+    for (int d = 0; d < c; ++d) s -= L[4 * c + d] * L[4 * c + d];
+    if (!(s > 0.0) || !isfinite(s)) ok = false;
+    pmax = fmax(pmax, s);
+    pmin = fmin(pmin, s);
+    const double l = sqrt(fmax(s, 1e-300));
+    L[4 * c + c] = l;
+    for (int r = c + 1; r < 4; ++r) {
+      double t = T[4 * r + c];
+      for (int d = 0; d < c; ++d) t -= L[4 * r + d] * L[4 * c + d];
+      L[4 * r + c] = t / l;
     }
-    double* zt = z + 6 * nb;
-    for (int c = 0; c < 4; ++c) {
-      double s = zt[c];
-      for (int d = 0; d < c; ++d) s -= L[4 * c + d] * zt[d];
-      zt[c] = s / L[4 * c + c];
-    }
-    for (int c = 3; c >= 0; --c) {
-      double s = zt[c];
-      for (int d = c + 1; d < 4; ++d) s -= L[4 * d + c] * zt[d];
-      zt[c] = s / L[4 * c + c];
-    }
-    A.cond[0] = pmax / fmax(pmin, 1e-300);
-    if (!ok) fail = 1;
   }
-  __syncthreads();
-  if (fail) {
-    if (tid == 0) A.status[0] = 1;
-    return;
+  for (int c = 0; c < 4; ++c) {
+    double s = zt[c];
+    for (int d = 0; d < c; ++d) s -= L[4 * c + d] * zt[d];
+    zt[c] = s / L[4 * c + c];
   }
-  // ---- backward (block LDL^T): x_b = D_b^-1 z_b - L_tb^T x_t - sum_{a>b} L_ab^T x_a.
-  // w_b = D_b^-1 z_b - L_tb^T x_t for all b in parallel (staged through delta), then
-  // one warp sweeps b = nb-1..0 folding x_b into the BW blocks above it.
-  for (int x = tid; x < 6 * nb; x += kSolveThreads) {
+  for (int c = 3; c >= 0; --c) {
+    double s = zt[c];
+    for (int d = c + 1; d < 4; ++d) s -= L[4 * d + c] * zt[d];
+    zt[c] = s / L[4 * c + c];
+  }
+  cond[0] = pmax / fmax(pmin, 1e-300);
+  return ok;
+}
+
+// Backward (block LDL^T): x_b = D_b^-1 z_b - L_tb^T x_t - sum_{a>b} L_ab^T x_a for
+// b < npiv.  On entry z[0, npiv) holds the forward rhs and z[npiv, nrows) the already
+// known x of the rows that were not pivoted; xt (4) the theta solution (calib).
+// `ring` (>= 8 factor rows) streams Lband rows via cp.async; tmp (6 npiv) staging.
+template <int NS>
+__device__ inline void chain_backward(double* z, const double* thL, const double* xt, const double* Lband,
+                                      double* ring, int nrows, int npiv, int BW, int calib, double* tmp) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int W1 = BW + 1, NR = W1 * 36;
+  for (int x = tid; x < 6 * npiv; x += kSolveThreads) {
     const int b = x / 6, s = x % 6;
-    const double* Di = A.Lband + ((size_t)b * W1 + BW) * 36 + 6 * s;
+    const double* Di = Lband + ((size_t)b * W1 + BW) * 36 + 6 * s;
     double v = 0.0;
 #pragma unroll
     for (int k = 0; k < 6; ++k) v = fma(Di[k], z[6 * b + k], v);
-    if (A.calib) {
+    if (calib) {
 #pragma unroll
-      for (int tt = 0; tt < 4; ++tt) v = fma(-thL[(size_t)b * 24 + 6 * tt + s], z[6 * nb + tt], v);
+      for (int tt = 0; tt < 4; ++tt) v = fma(-thL[(size_t)b * 24 + 6 * tt + s], xt[tt], v);
     }
-    A.delta[x] = v;
+    tmp[x] = v;
   }
   __syncthreads();
-  for (int x = tid; x < 6 * nb; x += kSolveThreads) z[x] = A.delta[x];
+  for (int x = tid; x < 6 * npiv; x += kSolveThreads) z[x] = tmp[x];
   __syncthreads();
-  if (crit && nb > 0) {
-    // register-prefetched factor row b: slot j of lane q = lane + 32 j (q < 6 BW)
-    // holds column s = q % 6 of L_{b, b-1-q/6}
-    double lc[NS][6], ln[NS][6];
-    auto fetch = [&](int b, double (&p)[NS][6]) {
-      const double* row = A.Lband + (size_t)(b < 0 ? 0 : b) * NR;
-#pragma unroll
-      for (int j = 0; j < NS; ++j) {
-        const int q = lane + 32 * j;
-        const bool ok = b >= 0 && q < 6 * BW && b - 1 - q / 6 >= 0;
-        const int pos = BW - 1 - q / 6, sc = q % 6;
-#pragma unroll
-        for (int k = 0; k < 6; ++k) p[j][k] = ok ? row[pos * 36 + 6 * k + sc] : 0.0;
+  if (warp == kCritWarp && nrows > 1) {
+    constexpr int RD = 8;
+    auto issue = [&](int a) {
+      if (a >= 1) {
+        const char* src = reinterpret_cast<const char*>(Lband + (size_t)a * NR);
+        const unsigned dst = (unsigned)__cvta_generic_to_shared(ring + (size_t)(a % RD) * NR);
+        for (int q = lane; q < NR / 2; q += 32)
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + 16 * q), "l"(src + 16 * q));
       }
+      asm volatile("cp.async.commit_group;");
     };
-    fetch(nb - 1, lc);
-    for (int b = nb - 1; b >= 0; --b) {
-      fetch(b - 1, ln);
+    for (int t = 0; t < RD; ++t) issue(nrows - 1 - t);
+    for (int a = nrows - 1; a >= 1; --a) {
+      asm volatile("cp.async.wait_group %0;" ::"n"(RD - 1) : "memory");
+      __syncwarp();
+      const double* row = ring + (size_t)(a % RD) * NR;
       double xr[6];
 #pragma unroll
-      for (int r = 0; r < 6; ++r) xr[r] = z[6 * b + r];
+      for (int r = 0; r < 6; ++r) xr[r] = z[6 * a + r];
 #pragma unroll
       for (int j = 0; j < NS; ++j) {
         const int q = lane + 32 * j;
-        if (q < 6 * BW && b - 1 - q / 6 >= 0) {
+        const int bp = a - 1 - q / 6;
+        if (q < 6 * BW && bp >= 0 && bp < npiv) {
+          const double* blk = row + (BW - 1 - q / 6) * 36 + q % 6;
           double acc = 0.0;
 #pragma unroll
-          for (int r = 0; r < 6; ++r) acc = fma(lc[j][r], xr[r], acc);
-          z[6 * (b - 1 - q / 6) + q % 6] -= acc;
+          for (int r = 0; r < 6; ++r) acc = fma(blk[6 * r], xr[r], acc);
+          z[6 * bp + q % 6] -= acc;
         }
       }
       __syncwarp();
-#pragma unroll
-      for (int j = 0; j < NS; ++j)
-#pragma unroll
-        for (int k = 0; k < 6; ++k) lc[j][k] = ln[j][k];
+      issue(a - RD);
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+  }
+  __syncthreads();
+}
+
+__device__ inline ChainSm chain_sm(unsigned char* smem, const SolveSmem& L, int* fail, bool middle) {
+  ChainSm S;
+  S.win = reinterpret_cast<double*>(smem + L.win);
+  S.th = reinterpret_cast<double*>(smem + (middle ? L.thm : L.th));
+  S.thL = reinterpret_cast<double*>(smem + (middle ? L.thLm : L.thL));
+  S.z = reinterpret_cast<double*>(smem + (middle ? L.zm : L.z));
+  S.dinv = reinterpret_cast<double*>(smem + L.dinv);
+  S.pbuf = reinterpret_cast<double*>(smem + L.pbuf);
+  S.cbuf = reinterpret_cast<double*>(smem + L.cbuf);
+  S.tbuf = reinterpret_cast<double*>(smem + L.tbuf);
+  S.pairs = reinterpret_cast<short2*>(smem + L.pairs);
+  S.fail = fail;
+  return S;
+}
+
+// one-sided solve (small systems)
+template <int NS>
+__global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const SolveArgs A) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const SolveSmem L = solve_smem_layout(A.nb, A.BW, A.calib);
+  __shared__ int fail;
+  const int tid = threadIdx.x;
+  const int nb = A.nb, BW = A.BW, NR = (BW + 1) * 36;
+  if (tid == 0) fail = 0;
+  const ChainSm S = chain_sm(smem, L, &fail, false);
+  const int r0 = min(BW, nb - 1);
+  for (int x = tid; x < (r0 + 1) * NR; x += kSolveThreads) S.win[x] = A.band[x];
+  if (A.calib) {
+    for (int x = tid; x < nb * 24; x += kSolveThreads) S.th[x] = A.theta[x];
+    if (tid < 16) S.th[nb * 24 + tid] = A.thth[tid];
+  }
+  for (int x = tid; x < 6 * nb + (A.calib ? 4 : 0); x += kSolveThreads) S.z[x] = A.y[x];
+  __syncthreads();
+  chain_forward(S, A.band, A.Lband, nb, nb, BW, A.calib, nb, A.lambda);
+  if (A.calib && tid == 0 && !fail)
+    if (!theta_solve(S.th + (size_t)nb * 24, S.z + 6 * nb, A.lambda, A.cond)) fail = 1;
+  __syncthreads();
+  if (fail) {
+    if (tid == 0) A.status[0] = 1;
+    return;
+  }
+  chain_backward<NS>(S.z, S.thL, S.z + 6 * nb, A.Lband, S.win, nb, nb, BW, A.calib, A.delta);
+  for (int x = tid; x < 6 * nb + (A.calib ? 4 : 0); x += kSolveThreads) A.delta[x] = S.z[x];
+}
+
+// two-sided solve: 2 cooperative CTAs (see the header comment)
+template <int NS>
+__global__ void __launch_bounds__(kSolveThreads, 1) solve2_kernel(const SolveArgs A) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ __align__(16) unsigned char smem[];
+  const SolveSmem L = solve_smem_layout(A.nb, A.BW, A.calib);
+  __shared__ int fail;
+  __shared__ double xts[4];
+  const int tid = threadIdx.x, cta = blockIdx.x;
+  const int nb = A.nb, BW = A.BW, W1 = BW + 1, NR = W1 * 36;
+  const int calib = A.calib;
+  const int m = A.m_top, mb = nb - m - BW;  // pivots of the top / bottom chain
+  const int npiv = cta == 0 ? m : mb;
+  const int nrows = npiv + BW;
+  const double* band = cta == 0 ? A.band : A.rband;
+  double* Lb = cta == 0 ? A.Lband : A.rLband;
+  if (tid == 0) fail = 0;
+  const ChainSm S = chain_sm(smem, L, &fail, false);
+  // ---- load this orientation: window rows, theta border, rhs (bottom: reversed)
+  for (int x = tid; x < W1 * NR; x += kSolveThreads) S.win[x] = band[x];
+  if (calib) {
+    for (int x = tid; x < nrows * 24; x += kSolveThreads) {
+      const int c = x / 24, e = x % 24;
+      S.th[x] = A.theta[(size_t)(cta == 0 ? c : nb - 1 - c) * 24 + e];
+    }
+    if (tid < 16) S.th[nb * 24 + tid] = A.thth[tid];
+  }
+  for (int x = tid; x < 6 * nrows; x += kSolveThreads) {
+    const int a = x / 6, s = x % 6;
+    S.z[x] = A.y[6 * (cta == 0 ? a : nb - 1 - a) + s];
+  }
+  if (calib && tid < 4) S.z[6 * nb + tid] = A.y[6 * nb + tid];
+  __syncthreads();
+  chain_forward(S, band, Lb, nrows, npiv, BW, calib, nb, A.lambda);
+  // ---- export the middle rows (local rows npiv..nrows-1, columns >= npiv)
+  const long long per = (long long)BW * BW * 36 + 6 * BW + (long long)BW * 24 + 16 + 4;
+  double* ex = A.mid + cta * per;
+  {
+    const int sb0 = npiv % W1;
+    for (int x = tid; x < BW * BW * 36; x += kSolveThreads) {
+      const int i = x / (BW * 36), j = (x / 36) % BW, e = x % 36;  // block (npiv+i, npiv+j)
+      double v = 0.0;
+      if (j <= i) {
+        int sl = sb0 + i;
+        sl = sl >= W1 ? sl - W1 : sl;
+        v = S.win[((size_t)sl * W1 + (j - i + BW)) * 36 + e];
+      }
+      ex[x] = v;
+    }
+    for (int x = tid; x < 6 * BW; x += kSolveThreads) ex[BW * BW * 36 + x] = S.z[6 * npiv + x];
+    if (calib) {
+      for (int x = tid; x < BW * 24; x += kSolveThreads)
+        ex[BW * BW * 36 + 6 * BW + x] = S.th[(size_t)npiv * 24 + x];
+      if (tid < 16) ex[BW * BW * 36 + 6 * BW + BW * 24 + tid] = S.th[nb * 24 + tid];
+      if (tid < 4) ex[BW * BW * 36 + 6 * BW + BW * 24 + 16 + tid] = S.z[6 * nb + tid];
     }
   }
-  SPROF(6);
+  int* gfail = A.status + 2;  // cross-CTA failure flag (reset by the host)
   __syncthreads();
-  SPROF(7);
-  for (int x = tid; x < nz; x += kSolveThreads) A.delta[x] = z[x];
-#ifdef DBA_SOLVE_PROF
-  if (lane == 0 && (warp == kCritWarp || warp == 0 || warp == 3)) {
-    const int base = warp == kCritWarp ? 0 : (warp == 0 ? 8 : 16);
-    for (int k = 0; k < 8; ++k) g_prof[base + k] = prof_acc[k] + (prof_sink == 12345);
+  if (tid == 0 && fail) atomicExch(gfail, 1);
+  __threadfence();
+  grid.sync();
+  double* xsol = A.mid + 2 * per + (long long)BW * BW * 36;  // 6 BW + 4
+  if (cta == 0 && *((volatile int*)gfail) == 0) {
+    // ---- middle system: T + B^T(reversed) - S over poses m..m+BW-1 (+ theta)
+    const ChainSm M = chain_sm(smem, L, &fail, true);
+    const double* T = A.mid;
+    const double* R = A.mid + per;
+    const int BWm = BW - 1, W1m = BW, NRm = W1m * 36;
+    for (int x = tid; x < BW * NRm; x += kSolveThreads) {
+      const int i = x / NRm, pos = (x % NRm) / 36, e = x % 36, r = e / 6, c = e % 6;
+      const int j = i - BWm + pos;  // column block (local middle index)
+      double v = 0.0;
+      if (j >= 0) {
+        const double t = T[((size_t)i * BW + j) * 36 + e];
+        const double rv = R[((size_t)(BW - 1 - j) * BW + (BW - 1 - i)) * 36 + 6 * c + r];
+        const double o = A.band[((size_t)(m + i) * W1 + (j - i + BW)) * 36 + e];
+        v = t + rv - o;
+      }
+      M.win[x] = v;
+    }
+    for (int x = tid; x < 6 * BW; x += kSolveThreads) {
+      const int i = x / 6, s = x % 6;
+      M.z[x] = T[BW * BW * 36 + x] + R[BW * BW * 36 + 6 * (BW - 1 - i) + s] - A.y[6 * (m + i) + s];
+    }
+    if (calib) {
+      for (int x = tid; x < BW * 24; x += kSolveThreads) {
+        const int i = x / 24, e = x % 24;
+        M.th[x] = T[BW * BW * 36 + 6 * BW + x] + R[BW * BW * 36 + 6 * BW + (BW - 1 - i) * 24 + e] -
+                  A.theta[(size_t)(m + i) * 24 + e];
+      }
+      const long long o2 = (long long)BW * BW * 36 + 6 * BW + BW * 24;
+      if (tid < 16) M.th[BW * 24 + tid] = T[o2 + tid] + R[o2 + tid] - A.thth[tid];
+      if (tid < 4) M.z[6 * BW + tid] = T[o2 + 16 + tid] + R[o2 + 16 + tid] - A.y[6 * nb + tid];
+    }
+    __syncthreads();
+    double* Lm = A.mid + 2 * per;
+    chain_forward(M, nullptr, Lm, BW, BW, BWm, calib, BW, A.lambda);
+    if (calib && tid == 0 && !fail)
+      if (!theta_solve(M.th + (size_t)BW * 24, M.z + 6 * BW, A.lambda, A.cond)) fail = 1;
+    __syncthreads();
+    if (!fail) chain_backward<NS>(M.z, M.thL, M.z + 6 * BW, Lm, M.win, BW, BW, BWm, calib, A.delta);
+    for (int x = tid; x < 6 * BW + (calib ? 4 : 0); x += kSolveThreads) xsol[x] = M.z[x];
+    __syncthreads();
+    if (tid == 0 && fail) atomicExch(gfail, 1);
   }
-#endif
+  __threadfence();
+  grid.sync();
+  if (*((volatile int*)gfail) != 0) {
+    if (tid == 0 && cta == 0) A.status[0] = 1;
+    return;
+  }
+  // ---- back-substitute this chain with the middle solution
+  for (int x = tid; x < 6 * BW; x += kSolveThreads) {
+    const int i = x / 6, s = x % 6;  // local middle row npiv + i
+    S.z[6 * npiv + x] = xsol[6 * (cta == 0 ? i : BW - 1 - i) + s];
+  }
+  if (tid < 4) xts[tid] = calib ? xsol[6 * BW + tid] : 0.0;
+  __syncthreads();
+  double* tmp = A.delta + (cta == 0 ? 0 : 6 * (m + BW));  // staging inside this chain's output range
+  chain_backward<NS>(S.z, S.thL, xts, Lb, S.win, nrows, npiv, BW, calib, tmp);
+  for (int x = tid; x < 6 * npiv; x += kSolveThreads) {
+    const int a = x / 6, s = x % 6;
+    A.delta[6 * (cta == 0 ? a : nb - 1 - a) + s] = S.z[x];
+  }
+  if (cta == 0) {
+    for (int x = tid; x < 6 * BW; x += kSolveThreads) A.delta[6 * m + x] = xsol[x];
+    if (calib && tid < 4) A.delta[6 * nb + tid] = xsol[6 * BW + tid];
+  }
 }
 
 }  // namespace dba

@@ -302,6 +302,8 @@ __global__ void __launch_bounds__(256) assemble_kernel(const AsmArgs A) {
 struct GatherUnit {
   long long dst;
   int rows, cols, c0, c1;
+  int trans = 0;  // square block written transposed (reversed band)
+  int pad = 0;
 };
 struct Contrib {
   long long src;
@@ -328,7 +330,7 @@ __global__ void gather_kernel(const GatherArgs A) {
     double s = 0.0;
     for (int q = u.c0; q < u.c1; ++q) {
       const Contrib cb = A.contrib[q];
-      s += A.Fbuf[cb.src + (long long)r * cb.stride + c];
+      s += u.trans ? A.Fbuf[cb.src + (long long)c * cb.stride + r] : A.Fbuf[cb.src + (long long)r * cb.stride + c];
     }
     A.sys[u.dst + e] = s;
   }

@@ -184,3 +184,26 @@ def test_solve_parity_calib(torch_cuda, iters):
     rel = _disp_err(Do.cpu().numpy().astype(np.float64), ref.disps, wl.disps0)
     assert np.quantile(rel, 0.999) < REL_TOL, np.quantile(rel, 0.999)
     assert rel.max() < 10 * REL_TOL, rel.max()
+
+
+@pytest.mark.parametrize("calib,keyframes,radius", [(False, 40, 2), (True, 40, 2), (False, 48, 3)])
+def test_two_sided_solve_parity(torch_cuda, calib, keyframes, radius):
+    """Long chains take the two-CTA (top/bottom) factorisation; same step as the oracle."""
+    name = "C5" if calib else "C3"
+    wl = small_workload(name, height=12, width=16, keyframes=keyframes, radius=radius)
+    s = _solver(wl, calib=calib)
+    assert s.info.solve_ctas == 2
+    lam = 1e-4
+    delta, pn, dn, kn, en = s.debug_trial(wl.poses0, wl.disps0, wl.intr0, wl.flow, lam=lam)
+    opts = O.Options(optimize_intrinsics=calib)
+    prob = oracle_problem(wl)
+    sysm = O.linearize(oracle_state(wl), prob, opts)
+    Sr, yr, _ = O.reduced(sysm, prob, opts)
+    dref, _ = O.solve_reduced(Sr, yr, lam)
+    assert _rel(delta, dref) < REL_TOL, _rel(delta, dref)
+    Po, Do, Ko, rep = s.solve(wl.poses0, wl.disps0, wl.intr0, wl.flow, iters=2)
+    ref, rrep = O.solve(oracle_state(wl), prob, O.Options(iters=2, optimize_intrinsics=calib))
+    assert rep.iterations_run == rrep.iterations
+    te, ae = pose_errors(Po.cpu().numpy(), ref.poses)
+    assert te < REL_TOL, te
+    assert abs(rep.final_energy - rrep.final_energy) <= REL_TOL * rrep.initial_energy
