@@ -62,7 +62,7 @@ constexpr size_t kAlign = 256;
 inline size_t align_up(size_t x) { return (x + kAlign - 1) & ~(kAlign - 1); }
 
 struct Readback {
-  int status[4];  // [0] factorisation failed, [1] bad edge (INT_MAX = none)
+  int status[4];  // flags word, see trial_skipped (dba_common.cuh)
   double cond;
   double energy;
   double pad[2];
@@ -75,7 +75,7 @@ struct Layout {
   size_t off_F, off_f, units, contrib, meta_end;
   // state
   size_t poses[2], intr[2], disps[2], xi, delta, lin, back, adj;
-  size_t part_edge, part_M, part_w, part_frame, Fbuf, sys[2], gstate[2], Lband, rLband, mid, flags, gauge, total;
+  size_t part_edge, part_M, part_w, part_frame, Fbuf, sys[2], gstate[2], Lband, rLband, mid, flags, ctl, gauge, total;
 };
 
 }  // namespace
@@ -95,6 +95,7 @@ struct dba_plan {
   std::vector<unsigned char> meta;  // image of [0, meta_end)
   unsigned char* meta_pinned = nullptr;
   Readback* rb = nullptr;
+  Control* ctl_h = nullptr;  // pinned mirror of the device GN controller
   const void* uploaded_ws = nullptr;
   int device = -1;
   // live kernel timing (dba_plan_set_profiling) and launch accounting
@@ -556,6 +557,7 @@ int dba_plan_create(const dba_problem_desc* d, dba_plan** out) {
   L.rLband = take(sizeof(double) * (p->two_sided ? p->band_len : 1));
   L.mid = take(sizeof(double) * (p->two_sided ? solve_mid_len(p->BW) : 1));
   L.flags = take(sizeof(Readback));
+  L.ctl = take(sizeof(Control));
   L.gauge = take(sizeof(double) * 4);
   L.total = o;
 
@@ -588,6 +590,7 @@ void dba_plan_destroy(dba_plan* p) {
   for (cudaEvent_t e : p->prof.pool) cudaEventDestroy(e);
   if (p->meta_pinned) cudaFreeHost(p->meta_pinned);
   if (p->rb) cudaFreeHost(p->rb);
+  if (p->ctl_h) cudaFreeHost(p->ctl_h);
   delete p;
 }
 
@@ -680,6 +683,7 @@ int prepare(Ctx& c) {
     DBA_CUDA(cudaMallocHost(&p->meta_pinned, std::max<size_t>(p->meta.size(), 1)));
     std::memcpy(p->meta_pinned, p->meta.data(), p->meta.size());
     DBA_CUDA(cudaMallocHost(&p->rb, sizeof(Readback)));
+    DBA_CUDA(cudaMallocHost(&p->ctl_h, sizeof(Control)));
   }
   if (p->uploaded_ws != c.b->workspace) {
     DBA_CUDA(cudaMemcpyAsync(c.ws, p->meta_pinned, p->meta.size(), cudaMemcpyHostToDevice, c.st));
@@ -842,14 +846,14 @@ int launch_system(Ctx& c, int slot) {
   return DBA_OK;
 }
 
-int launch_solve(Ctx& c, int slot, double lam) {
+int launch_solve(Ctx& c, int slot) {
   dba_plan* p = c.p;
   if (p->n_red == 0) return DBA_OK;
   SolveArgs a;
   a.nb = p->nb;
   a.BW = p->BW;
   a.calib = p->calib;
-  a.lambda = lam;
+  a.lambda = &c.at<Control>(p->L.ctl)->lam;
   a.status = c.at<int>(p->L.flags);
   const double* s = c.at<double>(p->L.sys[slot]);
   a.band = s;
@@ -888,6 +892,53 @@ int launch_solve(Ctx& c, int slot, double lam) {
     pr.solve_ev.push_back(ev);
   }
   return cuda_status(cudaGetLastError());
+}
+
+int launch_decide(Ctx& c) {
+  dba_plan* p = c.p;
+  DecideArgs a;
+  a.iters = c.o->iters;
+  a.calib = p->calib;
+  a.lam_min = c.o->lambda_min;
+  a.lam_max = c.o->lambda_max;
+  a.cond_max = c.o->calib_cond_max;
+  a.status = c.at<int>(p->L.flags);
+  a.cond = &c.at<Readback>(p->L.flags)->cond;
+  a.energy = c.at<double>(p->L.sys[1]) + p->energy_off;
+  a.ctl = c.at<Control>(p->L.ctl);
+  decide_kernel<<<1, 32, 0, c.st>>>(a);
+  p->prof.launches++;
+  return cuda_status(cudaGetLastError());
+}
+
+// accepted trial (slot 1) -> current iterate (slot 0)
+int launch_accept(Ctx& c) {
+  dba_plan* p = c.p;
+  AcceptArgs a;
+  a.ctl = c.at<Control>(p->L.ctl);
+  a.nspan = 0;
+  auto span = [&](size_t dst, size_t src, long long words) {
+    a.span[a.nspan++] = CopySpan{c.at<float>(dst), c.at<float>(src), words};
+  };
+  span(p->L.poses[0], p->L.poses[1], 14LL * p->N);
+  span(p->L.intr[0], p->L.intr[1], 8);
+  span(p->L.disps[0] + sizeof(float) * (size_t)p->f0 * p->P, p->L.disps[1] + sizeof(float) * (size_t)p->f0 * p->P,
+       (long long)p->NL * p->P);
+  span(p->L.sys[0], p->L.sys[1], 2 * p->sys_len);
+  span(p->L.gstate[0], p->L.gstate[1], 2LL * (6 * kMaxOutDegree + 8));
+  accept_kernel<<<2 * std::max(p->G, 1), 256, 0, c.st>>>(a);
+  p->prof.launches++;
+  return cuda_status(cudaGetLastError());
+}
+
+int upload_control(Ctx& c, double lam, double Ec) {
+  Control h{};
+  h.lam = lam;
+  h.Ec = Ec;
+  h.bad_edge = -1;
+  *c.p->ctl_h = h;
+  DBA_CUDA(cudaMemcpyAsync(c.at<Control>(c.p->L.ctl), c.p->ctl_h, sizeof(Control), cudaMemcpyHostToDevice, c.st));
+  return DBA_OK;
 }
 
 int reset_flags(Ctx& c) {
@@ -972,44 +1023,46 @@ int dba_solve(dba_plan* p, const dba_options* o, const dba_buffers* b, dba_repor
   }
   double Ec = rb.energy;
   rep->initial_energy = Ec;
-  double lam = o->lambda0;
-  int cur = 0, it = 0;
-  while (it < o->iters) {
-    const int nxt = 1 - cur;
-    if ((s = reset_flags(c))) return rep->status = s;
-    if ((s = launch_solve(c, cur, lam))) return rep->status = s;
-    if ((s = launch_prep(c, cur, nxt, false))) return rep->status = s;
-    if ((s = launch_pass(c, cur, nxt, true, true))) return rep->status = s;
-    if ((s = launch_system(c, nxt))) return rep->status = s;
-    if ((s = read_flags(c, nxt, rb))) return rep->status = s;
-    if (rb.status[0] != 0) {  // factorisation failed: more damping
-      lam *= 10.0;
-      if (lam > o->lambda_max) return rep->status = DBA_ESOLVER;
-      continue;
+  // The whole LM schedule is enqueued without host round trips (decide_kernel);
+  // batches of trials are launched until the controller reports done.  Kernels of
+  // trials queued past the end return at entry.
+  if ((s = upload_control(c, o->lambda0, Ec))) return rep->status = s;
+  Control ctl{};
+  ctl.lam = o->lambda0;
+  ctl.Ec = Ec;
+  ctl.bad_edge = -1;
+  for (int seen = 0; o->iters > 0;) {
+    const int batch = std::max(1, o->iters - seen);
+    for (int t = 0; t < batch; ++t) {
+      if ((s = launch_solve(c, 0))) return rep->status = s;
+      if ((s = launch_prep(c, 0, 1, false))) return rep->status = s;
+      if ((s = launch_pass(c, 0, 1, true, true))) return rep->status = s;
+      if ((s = launch_system(c, 1))) return rep->status = s;
+      if ((s = launch_decide(c))) return rep->status = s;
+      if ((s = launch_accept(c))) return rep->status = s;
     }
-    rep->trials++;
-    if (p->calib) {
-      rep->calib_condition = rb.cond;
-      if (o->calib_cond_max > 0 && rb.cond > o->calib_cond_max) return rep->status = DBA_ECALIB;
-    }
-    if (rb.status[1] != INT_MAX || !std::isfinite(rb.energy)) {
-      rep->bad_edge = rb.status[1] != INT_MAX ? rb.status[1] : -1;
-      return rep->status = DBA_ENONFINITE;
-    }
-    if (rb.energy <= Ec) {
-      cur = nxt;
-      Ec = rb.energy;
-      lam = std::max(lam / 10.0, o->lambda_min);
-      if (rep->trace_len < DBA_TRACE_MAX) rep->energy_trace[rep->trace_len++] = Ec;
-      ++it;
-    } else {
-      lam *= 10.0;
-      if (lam > o->lambda_max) {
-        rep->converged = 1;
-        break;
-      }
-    }
+    DBA_CUDA(cudaMemcpyAsync(p->ctl_h, c.at<Control>(p->L.ctl), sizeof(Control), cudaMemcpyDeviceToHost, c.st));
+    DBA_CUDA(cudaStreamSynchronize(c.st));
+    ctl = *p->ctl_h;
+    if (p->prof.on) prof_resolve(p);
+    if (ctl.done) break;
+    seen = ctl.it;
   }
+  rep->trials = ctl.trials;
+  rep->calib_condition = ctl.cond;
+  rep->trace_len = std::min(ctl.it, DBA_TRACE_MAX);
+  for (int i = 0; i < rep->trace_len; ++i) rep->energy_trace[i] = ctl.trace[i];
+  if (ctl.result == 1) return rep->status = DBA_ESOLVER;
+  if (ctl.result == 2) return rep->status = DBA_ECALIB;
+  if (ctl.result == 3) {
+    rep->bad_edge = ctl.bad_edge;
+    return rep->status = DBA_ENONFINITE;
+  }
+  rep->converged = ctl.converged;
+  const int it = ctl.it;
+  const int cur = 0;
+  Ec = ctl.Ec;
+  const double lam = ctl.lam;
   rep->iterations = it;
   rep->final_energy = Ec;
   rep->lambda_final = lam;
@@ -1134,7 +1187,8 @@ int dba_debug_trial(dba_plan* p, const dba_options* o, const dba_buffers* b, dou
   if ((s = prepare(c))) return s;
   if ((s = initial_pass(c))) return s;
   if ((s = reset_flags(c))) return s;
-  if ((s = launch_solve(c, 0, lambda))) return s;
+  if ((s = upload_control(c, lambda, 0.0))) return s;
+  if ((s = launch_solve(c, 0))) return s;
   if ((s = launch_prep(c, 0, 1, false))) return s;
   if ((s = launch_pass(c, 0, 1, true, true))) return s;
   if ((s = launch_system(c, 1))) return s;

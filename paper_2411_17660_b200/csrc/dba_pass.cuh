@@ -48,7 +48,7 @@ struct PassArgs {
   int backsub;  // run phase A
   int system;   // produce system partials (0: energy only)
   int stage;    // flow records of the next sub-tile are staged in smem with cp.async
-  const int* status;  // abort when status[0] != 0 (failed factorisation)
+  const int* status;  // see trial_skipped
   const int* csr_off;
   const int* slot_flow;
   const int* frame_of;
@@ -167,7 +167,7 @@ __device__ __forceinline__ PixTerms pix_terms(const float R[9], const float t[3]
 
 template <bool CALIB>
 __global__ void __launch_bounds__(kPassThreads, 1) pass_kernel(const PassArgs A) {
-  if (A.status != nullptr && A.status[0] != 0) return;
+  if (trial_skipped(A.status)) return;
   extern __shared__ __align__(16) unsigned char smem[];
   constexpr int NVE = kEdgeVals + (CALIB ? kCalibVals : 0);
   const PassSmem L = pass_smem_layout(A.kmax, CALIB, A.stage != 0);

@@ -42,7 +42,7 @@ constexpr int kMaxBand = 24;        // compiled limit on BW
 
 struct SolveArgs {
   int nb, BW, calib;
-  double lambda;
+  const double* lambda;  // damping (device: the GN controller's current value)
   int* status;
   const double* band;   // nb*(BW+1)*36, block (a,c) at (a*(BW+1) + c-a+BW)*36
   const double* rband;  // the same band in reversed block order (two-sided solve)
@@ -506,6 +506,8 @@ __device__ inline ChainSm chain_sm(unsigned char* smem, const SolveSmem& L, int*
 // one-sided solve (small systems)
 template <int NS>
 __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const SolveArgs A) {
+  if (A.status[3] != 0) return;  // GN loop finished
+  const double lam = *A.lambda;
   extern __shared__ __align__(16) unsigned char smem[];
   const SolveSmem L = solve_smem_layout(A.nb, A.BW, A.calib);
   __shared__ int fail;
@@ -521,9 +523,9 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const SolveArgs
   }
   for (int x = tid; x < 6 * nb + (A.calib ? 4 : 0); x += kSolveThreads) S.z[x] = A.y[x];
   __syncthreads();
-  chain_forward(S, A.band, A.Lband, nb, nb, BW, A.calib, nb, A.lambda);
+  chain_forward(S, A.band, A.Lband, nb, nb, BW, A.calib, nb, lam);
   if (A.calib && tid == 0 && !fail)
-    if (!theta_solve(S.th + (size_t)nb * 24, S.z + 6 * nb, A.lambda, A.cond)) fail = 1;
+    if (!theta_solve(S.th + (size_t)nb * 24, S.z + 6 * nb, lam, A.cond)) fail = 1;
   __syncthreads();
   if (fail) {
     if (tid == 0) A.status[0] = 1;
@@ -538,6 +540,8 @@ template <int NS>
 __global__ void __launch_bounds__(kSolveThreads, 1) solve2_kernel(const SolveArgs A) {
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
+  if (A.status[3] != 0) return;  // GN loop finished (uniform over both CTAs)
+  const double lam = *A.lambda;
   extern __shared__ __align__(16) unsigned char smem[];
   const SolveSmem L = solve_smem_layout(A.nb, A.BW, A.calib);
   __shared__ int fail;
@@ -567,7 +571,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve2_kernel(const SolveArg
   }
   if (calib && tid < 4) S.z[6 * nb + tid] = A.y[6 * nb + tid];
   __syncthreads();
-  chain_forward(S, band, Lb, nrows, npiv, BW, calib, nb, A.lambda);
+  chain_forward(S, band, Lb, nrows, npiv, BW, calib, nb, lam);
   // ---- export the middle rows (local rows npiv..nrows-1, columns >= npiv)
   const long long per = (long long)BW * BW * 36 + 6 * BW + (long long)BW * 24 + 16 + 4;
   double* ex = A.mid + cta * per;
@@ -631,9 +635,9 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve2_kernel(const SolveArg
     }
     __syncthreads();
     double* Lm = A.mid + 2 * per;
-    chain_forward(M, nullptr, Lm, BW, BW, BWm, calib, BW, A.lambda);
+    chain_forward(M, nullptr, Lm, BW, BW, BWm, calib, BW, lam);
     if (calib && tid == 0 && !fail)
-      if (!theta_solve(M.th + (size_t)BW * 24, M.z + 6 * BW, A.lambda, A.cond)) fail = 1;
+      if (!theta_solve(M.th + (size_t)BW * 24, M.z + 6 * BW, lam, A.cond)) fail = 1;
     __syncthreads();
     if (!fail) chain_backward<NS>(M.z, M.thL, M.z + 6 * BW, Lm, M.win, BW, BW, BWm, calib, A.delta);
     for (int x = tid; x < 6 * BW + (calib ? 4 : 0); x += kSolveThreads) xsol[x] = M.z[x];

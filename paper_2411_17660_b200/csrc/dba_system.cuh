@@ -10,6 +10,8 @@
 //   gauge kernels    A5 scale gauge at the end of a solve
 #pragma once
 
+#include <climits>
+
 #include "dba_common.cuh"
 
 namespace dba {
@@ -58,7 +60,7 @@ __device__ inline Pose64 stepped_pose(const PrepArgs& A, int k, const double xi[
 }
 
 __global__ void prep_kernel(const PrepArgs A) {
-  if (A.status != nullptr && A.status[0] != 0) return;
+  if (trial_skipped(A.status)) return;
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t < A.N) {
     double xi[6];
@@ -153,7 +155,7 @@ __device__ __forceinline__ int tri4(int r, int c) {
 }
 
 __global__ void __launch_bounds__(256) assemble_kernel(const AsmArgs A) {
-  if (A.status != nullptr && A.status[0] != 0) return;
+  if (trial_skipped(A.status)) return;
   __shared__ double Ad[kMaxOutDegree * 36];
   __shared__ double hs[kMaxOutDegree * (kEdgeVals + kCalibVals)];
   __shared__ double ws[6 * kMaxOutDegree + 4];
@@ -320,7 +322,7 @@ struct GatherArgs {
 };
 
 __global__ void gather_kernel(const GatherArgs A) {
-  if (A.status != nullptr && A.status[0] != 0) return;
+  if (trial_skipped(A.status)) return;
   const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (wid >= A.n_units) return;
   const GatherUnit u = A.units[wid];
@@ -346,7 +348,7 @@ struct FinalArgs {
 };
 
 __global__ void __launch_bounds__(256) finalize_kernel(const FinalArgs A) {
-  if (A.status != nullptr && A.status[0] != 0) return;
+  if (trial_skipped(A.status)) return;
   __shared__ double sh[256];
   double s = 0.0;
   for (int x = threadIdx.x; x < A.n; x += 256) s += A.part_frame[(long long)x * kFrameVals];
@@ -406,6 +408,105 @@ __global__ void gauge_apply_kernel(const GaugeArgs A) {
     for (int r = 0; r < 3; ++r) w[r] = Rg[r] * pg.t[0] + Rg[3 + r] * pg.t[1] + Rg[6 + r] * pg.t[2];
     for (int r = 0; r < 3; ++r) c[r] = Rk[3 * r] * w[0] + Rk[3 * r + 1] * w[1] + Rk[3 * r + 2] * w[2];
     for (int r = 0; r < 3; ++r) A.poses[7 * t + 4 + r] = (pk.t[r] - c[r]) / s + c[r];
+  }
+}
+
+}  // namespace dba
+
+namespace dba {
+
+// ---------------------------------------------------------------- GN controller
+// The Levenberg-Marquardt schedule (A1) runs on the device so that a
+// whole solve is enqueued without host round trips: state slot 0 is the current
+// iterate, slot 1 the trial; decide_kernel accepts / rejects and accept_kernel
+// copies an accepted trial over the current iterate.
+constexpr int kTraceMax = 64;  // == DBA_TRACE_MAX
+
+struct Control {
+  double lam, Ec, cond;
+  int it, trials, result, converged, bad_edge, accept, done, pad;
+  double trace[kTraceMax];
+};
+
+struct DecideArgs {
+  int iters, calib;
+  double lam_min, lam_max, cond_max;
+  int* status;          // flags word
+  double* cond;         // theta pivot ratio of the last solve
+  const double* energy; // energy of the trial state (slot 1)
+  Control* ctl;
+};
+
+__global__ void decide_kernel(const DecideArgs A) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  Control* c = A.ctl;
+  int* st = A.status;
+  c->accept = 0;
+  if (st[3] != 0) return;
+  int done = 0;
+  if (st[0] != 0) {  // factorisation failed: more damping, same iterate
+    c->lam *= 10.0;
+    if (c->lam > A.lam_max) {
+      c->result = 1;  // DBA_ESOLVER (mapped by the host)
+      done = 1;
+    }
+  } else {
+    c->trials++;
+    const double E = *A.energy;
+    if (A.calib) {
+      c->cond = *A.cond;
+      if (A.cond_max > 0.0 && c->cond > A.cond_max) {
+        c->result = 2;  // DBA_ECALIB
+        done = 1;
+      }
+    }
+    if (!done && (st[1] != INT_MAX || !isfinite(E))) {
+      c->bad_edge = st[1] != INT_MAX ? st[1] : -1;
+      c->result = 3;  // DBA_ENONFINITE
+      done = 1;
+    }
+    if (!done) {
+      if (E <= c->Ec) {
+        c->accept = 1;
+        c->Ec = E;
+        c->lam = fmax(c->lam / 10.0, A.lam_min);
+        if (c->it < kTraceMax) c->trace[c->it] = E;
+        c->it++;
+        if (c->it >= A.iters) done = 1;
+      } else {
+        c->lam *= 10.0;
+        if (c->lam > A.lam_max) {
+          c->converged = 1;
+          done = 1;
+        }
+      }
+    }
+  }
+  c->done = done;
+  st[0] = 0;
+  st[1] = INT_MAX;
+  st[2] = 0;
+  st[3] = done;
+  *A.cond = 0.0;
+}
+
+struct CopySpan {
+  float* dst;
+  const float* src;
+  long long n;  // 4-byte words
+};
+struct AcceptArgs {
+  const Control* ctl;
+  CopySpan span[5];
+  int nspan;
+};
+
+__global__ void accept_kernel(const AcceptArgs A) {
+  if (!A.ctl->accept) return;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (int s = 0; s < A.nspan; ++s) {
+    const CopySpan sp = A.span[s];
+    for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < sp.n; x += stride) sp.dst[x] = sp.src[x];
   }
 }
 
