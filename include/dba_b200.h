@@ -33,8 +33,10 @@
  *    edges (all edges when nranks == 1).
  *  - Errors: every entry point returns a DBA_* status; no C++ exception
  *    crosses the ABI.  DBA_ENONFINITE sets report->bad_edge (input edge id).
- *  - Threading: stream-ordered on `stream`; dba_solve synchronises the stream
- *    once per Gauss-Newton trial to read the accept/reject energy.  Distinct
+ *  - Threading: stream-ordered on `stream`.  The Levenberg-Marquardt
+ *    accept/reject schedule runs on the device; dba_solve enqueues batches of
+ *    trials and synchronises the stream once per batch (once per call when no
+ *    trial is rejected) to read the controller state.  Distinct
  *    plans + workspaces may run concurrently on distinct streams; one plan
  *    must not be used concurrently.
  *  - Determinism: fixed reduction trees, no floating-point atomics; results
@@ -61,6 +63,7 @@ extern "C" {
 #define DBA_ECALIB 5       /* CalibrationDegenerateError */
 #define DBA_ECUDA 6        /* CUDA runtime failure */
 #define DBA_ENCCL 7        /* NCCL failure */
+#define DBA_EDATA 8        /* DataError: missing / malformed DSPT provider file */
 
 #define DBA_TRACE_MAX 64
 
@@ -168,7 +171,7 @@ int dba_build_system(dba_plan* plan, const dba_options* opt, const dba_buffers* 
 
 /* Launch accounting and live kernel timing.  With profiling enabled the library
  * brackets every fused-pass and solve launch with CUDA events on the launching
- * stream and accumulates their durations (resolved at each per-trial sync). */
+ * stream and accumulates their durations (resolved at each stream sync). */
 typedef struct {
   int64_t launches;        /* all kernels launched by the library */
   int64_t pass_launches;   /* fused linearise/back-substitute passes */
@@ -190,6 +193,55 @@ int dba_debug_trial(dba_plan* plan, const dba_options* opt, const dba_buffers* b
 int dba_nccl_unique_id(uint8_t id_out[128]);
 int dba_nccl_comm_init(int32_t nranks, const uint8_t id[128], int32_t rank, void** comm_out);
 int dba_nccl_comm_destroy(void* comm);
+
+/* Provider-tensor ingestion (replaces PrecomputedProviders, providers.py:401-424).
+ * DSPT files (providers.py:12-15, :368-399): "DSPT", u32 version = 1, u32 H, W,
+ * C, then H*W*C little-endian float32.  Flow files <dir>/flow_{i:06d}_{j:06d}.dspt
+ * (C = 4) land directly in the dba_buffers.flow layout, record e = edge
+ * (ii[e], jj[e]), with the weights clipped to [0, 1] as provide_correspondences
+ * does (:415-420; NaN kept).  Priors <dir>/prior_{k:06d}.dspt (C = 1) are clamped
+ * below at 1e-6 (:422-424).  A missing, malformed (magic, version, length), or
+ * wrong-shape file returns DBA_EDATA with the smallest failing index in *bad_*.
+ * n_threads <= 0: one reader per hardware thread. */
+int dba_dspt_read_flows(const char* directory, int32_t n_edges, const int32_t* ii, const int32_t* jj, int32_t H,
+                        int32_t W, float* out_host, int32_t n_threads, int32_t* bad_edge);
+int dba_dspt_read_priors(const char* directory, int32_t n_frames, const int32_t* frames, int32_t H, int32_t W,
+                         float* out_host, int32_t n_threads, int32_t* bad_frame);
+/* Same flow records into DEVICE memory: file reads fill one half of the
+ * caller's pinned `staging` buffer while the other half is copied
+ * asynchronously on `stream`; staging_bytes must hold >= 2 records
+ * (2 * 16 * H * W bytes).  Returns after the last copy has completed. */
+int dba_dspt_load_flows(const char* directory, int32_t n_edges, const int32_t* ii, const int32_t* jj, int32_t H,
+                        int32_t W, float* out_device, void* staging, int64_t staging_bytes, int32_t n_threads,
+                        void* stream, int32_t* bad_edge);
+
+/* Frame-graph construction (the map_state
+ * operations that produce ii/jj).  Conventions G1-G4: oracle/graph.py, DESIGN.md.
+ *
+ * dba_frame_distance: mean_flow_distance for n_pairs ordered
+ * pairs (ia[k] -> ib[k]) of frames in poses (N,7) / disps (N,H,W) / intr (4,):
+ * beta * mean |full flow| + (1 - beta) * mean |rotation-only flow| over frame
+ * ia's pixels in front of the camera.  DEVICE pointers; out (n_pairs,) float64;
+ * float64 without contraction in a fixed reduction order (bitwise reproducible).
+ * Stream-ordered, no synchronisation. */
+int dba_frame_distance(int32_t n_frames, int32_t H, int32_t W, const double* poses, const float* disps,
+                       const double* intr, int32_t n_pairs, const int32_t* ia, const int32_t* ib, double beta,
+                       double* out, void* stream);
+/* build_frontend_edges: ordered pairs of the window at most
+ * `radius` apart (window order) plus existing in-window edges, minus edges whose
+ * age exceeds max_age; sorted by (i, j).  HOST pointers; age may be NULL.
+ * Writes up to `capacity` edges, *n_out = total (DBA_ECAPACITY if larger). */
+int dba_frontend_edges(int32_t n_window, const int32_t* window, int32_t radius, int32_t n_existing,
+                       const int32_t* ei, const int32_t* ej, const int32_t* age, int32_t max_age, int32_t capacity,
+                       int32_t* out_i, int32_t* out_j, int32_t* n_out);
+/* build_backend_graph: over the last `window` of the n_frames
+ * keyframes `frames` (ascending), unordered pairs ranked by (mean of the two
+ * directed distances dist[a*n+b], dist[b*n+a]; frames[a]; frames[b]), each adding
+ * both directions, loop edges always kept, at most max_edges edges; sorted by
+ * (i, j).  HOST pointers; dist is (n_frames, n_frames) float64. */
+int dba_backend_edges(int32_t n_frames, const int32_t* frames, const double* dist, int32_t window, int32_t max_edges,
+                      int32_t n_loop, const int32_t* li, const int32_t* lj, int32_t capacity, int32_t* out_i,
+                      int32_t* out_j, int32_t* n_out);
 
 #ifdef __cplusplus
 }

@@ -19,7 +19,7 @@ __all__ = [
 
 def __getattr__(name):
     # the solver API imports torch + the CUDA library lazily
-    if name in ("dba", "scenes", "geometry"):
+    if name in ("dba", "scenes", "geometry", "ingest"):
         import importlib
         return importlib.import_module(f".{name}", __name__)
     raise AttributeError(name)

@@ -23,6 +23,7 @@ DBA_ESOLVER = 4
 DBA_ECALIB = 5
 DBA_ECUDA = 6
 DBA_ENCCL = 7
+DBA_EDATA = 8
 TRACE_MAX = 64
 
 c_i32 = ctypes.c_int32
@@ -86,6 +87,8 @@ EXPORTS = (
     "dba_version", "dba_status_string", "dba_partition", "dba_plan_create", "dba_plan_destroy",
     "dba_plan_get_info", "dba_plan_local_edges", "dba_solve", "dba_energy", "dba_build_system",
     "dba_plan_set_profiling", "dba_plan_get_stats", "dba_debug_trial", "dba_nccl_unique_id", "dba_nccl_comm_init", "dba_nccl_comm_destroy",
+    "dba_dspt_read_flows", "dba_dspt_read_priors", "dba_dspt_load_flows",
+    "dba_frame_distance", "dba_frontend_edges", "dba_backend_edges",
 )
 
 _lib = None
@@ -142,6 +145,24 @@ def load():
     lib.dba_nccl_comm_init.argtypes = [c_i32, P(ctypes.c_uint8), c_i32, P(c_vp)]
     lib.dba_nccl_comm_destroy.restype = c_i32
     lib.dba_nccl_comm_destroy.argtypes = [c_vp]
+    Pf = P(ctypes.c_float)
+    lib.dba_dspt_read_flows.restype = c_i32
+    lib.dba_dspt_read_flows.argtypes = [ctypes.c_char_p, c_i32, P(c_i32), P(c_i32), c_i32, c_i32, Pf, c_i32,
+                                        P(c_i32)]
+    lib.dba_dspt_read_priors.restype = c_i32
+    lib.dba_dspt_read_priors.argtypes = [ctypes.c_char_p, c_i32, P(c_i32), c_i32, c_i32, Pf, c_i32, P(c_i32)]
+    lib.dba_dspt_load_flows.restype = c_i32
+    lib.dba_dspt_load_flows.argtypes = [ctypes.c_char_p, c_i32, P(c_i32), P(c_i32), c_i32, c_i32, c_vp, c_vp,
+                                        ctypes.c_int64, c_i32, c_vp, P(c_i32)]
+    lib.dba_frame_distance.restype = c_i32
+    lib.dba_frame_distance.argtypes = [c_i32, c_i32, c_i32, c_vp, c_vp, c_vp, c_i32, c_vp, c_vp, c_dbl, c_vp,
+                                       c_vp]
+    lib.dba_frontend_edges.restype = c_i32
+    lib.dba_frontend_edges.argtypes = [c_i32, P(c_i32), c_i32, c_i32, P(c_i32), P(c_i32), P(c_i32), c_i32,
+                                       c_i32, P(c_i32), P(c_i32), P(c_i32)]
+    lib.dba_backend_edges.restype = c_i32
+    lib.dba_backend_edges.argtypes = [c_i32, P(c_i32), P(c_dbl), c_i32, c_i32, c_i32, P(c_i32), P(c_i32),
+                                      c_i32, P(c_i32), P(c_i32), P(c_i32)]
     _lib = lib
     return lib
 

@@ -164,6 +164,7 @@ const char* dba_status_string(int s) {
     case DBA_ECALIB: return "intrinsics degenerate (poorly conditioned)";
     case DBA_ECUDA: return "CUDA error";
     case DBA_ENCCL: return "NCCL error";
+    case DBA_EDATA: return "missing or malformed DSPT provider file";
     default: return "unknown status";
   }
 }
