@@ -81,6 +81,8 @@ typedef struct {
   int32_t use_prior;           /* energy_rgbd term */
   int32_t scale_gauge;         /* -1 auto (1 fixed pose, no prior), 0 off, 1 on */
   int32_t rank, nranks;        /* edge sharding by source frame */
+  int32_t freeze_disparities;  /* disparity block not updated (SPEC BAProblem block flags):
+                                  motion-only pose solves, fill_nonkeyframe_poses */
 } dba_problem_desc;
 
 /* Solver knobs. */
@@ -110,6 +112,8 @@ typedef struct {
   size_t workspace_bytes;
   void* stream;             /* cudaStream_t (NULL = legacy default stream) */
   void* nccl_comm;          /* ncclComm_t for nranks > 1, else NULL */
+  const float* prior_weight;/* (N,) per-frame multiplier of alpha, or NULL (= 1); the Eq. 5
+                               affine prior s d + o = d* enters as d*' = (d* - o)/s, weight s^2 */
 } dba_buffers;
 
 /* SPEC BAReport + diagnostics. */
@@ -242,6 +246,20 @@ int dba_frontend_edges(int32_t n_window, const int32_t* window, int32_t radius, 
 int dba_backend_edges(int32_t n_frames, const int32_t* frames, const double* dist, int32_t window, int32_t max_edges,
                       int32_t n_loop, const int32_t* li, const int32_t* lj, int32_t capacity, int32_t* out_i,
                       int32_t* out_j, int32_t* n_out);
+
+/* P-RGBD block-coordinate descent, Eq. 5
+ * E_reg,m = alpha sum m (d* - (s_i d + o_i))^2 with per-frame scale/offset.
+ * dba_prior_affine: stage A (s, o frozen) input to dba_solve — prior_out =
+ *   (d* - o) / s (N,P) and weight_out = s^2 (N,) for dba_buffers.prior /
+ *   prior_weight (same energy and normal equations).
+ * dba_fit_affine: stage B closed form — per frame the 2x2 least-squares (s, o)
+ *   over mask pixels given disps, in place; s clamped to >= s_min; frames with
+ *   no mask pixel keep (s, o); constant-disparity frames keep s.
+ * DEVICE pointers, stream-ordered; scale/offset are (N,) float64. */
+int dba_prior_affine(int32_t n_frames, int32_t n_pixels, const float* prior, const double* scale,
+                     const double* offset, float* prior_out, float* weight_out, void* stream);
+int dba_fit_affine(int32_t n_frames, int32_t n_pixels, const float* disps, const float* prior, const uint8_t* mask,
+                   double* scale, double* offset, double s_min, void* stream);
 
 #ifdef __cplusplus
 }

@@ -95,6 +95,8 @@ class Problem:
     fixed: np.ndarray  # (N,) bool
     prior: np.ndarray | None = None  # (N,H,W) disparity prior d*
     prior_mask: np.ndarray | None = None  # (N,H,W) {0,1}
+    prior_weight: np.ndarray | None = None  # (N,) multiplier of alpha (Eq. 5 stage A: s^2)
+    freeze_disparities: bool = False  # disparity block not updated (motion-only)
 
     @property
     def n_edges(self):
@@ -271,10 +273,18 @@ def _frame_terms(state, prob, opts, i, edges, calib, want_hessian):
         dstar = prob.prior[i].reshape(-1).astype(np.float64)
         msk = prob.prior_mask[i].reshape(-1).astype(np.float64)
         dcur = state.disps[i].reshape(-1)
-        C += opts.alpha * msk
-        gd += opts.alpha * msk * (dstar - dcur)
-        energy += float(opts.alpha * np.sum(msk * (dstar - dcur) ** 2))
+        al = prior_alpha(prob, opts, i)
+        C += al * msk
+        gd += al * msk * (dstar - dcur)
+        energy += float(al * np.sum(msk * (dstar - dcur) ** 2))
     return U, C, gd, energy, eng_e, fin_e, blocks, grads
+
+
+def prior_alpha(prob: Problem, opts: Options, i: int) -> float:
+    """alpha of frame i's prior term (times the per-frame weight when given)."""
+    if prob.prior_weight is None:
+        return opts.alpha
+    return opts.alpha * float(prob.prior_weight[i])
 
 
 def _local_index(N, i, jlist):
@@ -329,8 +339,8 @@ def linearize(state: State, prob: Problem, opts: Options, frames=None,
             y[rs] += g
         Cs[i] = C
         gds[i] = gd
-        if not edges and not calib:
-            continue
+        if (not edges and not calib) or prob.freeze_disparities:
+            continue  # frozen disparities: no Schur fill-in, B and g stand alone
         idx = _local_index(N, i, [int(prob.jj[e]) for e in edges])
         Uc = U / C[:, None]
         S[np.ix_(idx, idx)] -= U.T @ Uc
@@ -371,7 +381,7 @@ def energy(state: State, prob: Problem, opts: Options | None = None) -> float:
     if prob.prior is not None:
         for i in range(N):
             dd = prob.prior[i].astype(np.float64) - state.disps[i]
-            tot += float(opts.alpha * np.sum(prob.prior_mask[i] * dd * dd))
+            tot += float(prior_alpha(prob, opts, i) * np.sum(prob.prior_mask[i] * dd * dd))
     return tot
 
 
@@ -430,6 +440,8 @@ def backsub_and_retract(state: State, prob: Problem, opts: Options, dxi_all, dth
     frame_list = range(N) if frames is None else frames
     g_frame = gauge_frame(prob, opts)
     for i in frame_list:
+        if prob.freeze_disparities:
+            continue
         edges = [int(x) for x in order[offs[i]:offs[i + 1]]]
         U, C, gd, *_ = _frame_terms(state, prob, opts, i, edges, calib, False)
         loc = [dxi_all[i]] + [dxi_all[int(prob.jj[e])] for e in edges]
@@ -463,6 +475,8 @@ def split_step(delta, fixed, calib):
 
 
 def use_scale_gauge(prob: Problem, opts: Options):
+    if prob.freeze_disparities:
+        return False
     if opts.scale_gauge is not None:
         return bool(opts.scale_gauge)
     return int(np.sum(prob.fixed)) == 1 and prob.prior is None
@@ -584,8 +598,8 @@ def dense_joint_step(state: State, prob: Problem, opts: Options, lam: float):
             m = prob.prior_mask[i].reshape(-1)
             dd = prob.prior[i].reshape(-1) - state.disps[i].reshape(-1)
             for p in range(P):
-                H[dof + i * P + p, dof + i * P + p] += opts.alpha * m[p]
-                g[dof + i * P + p] += opts.alpha * m[p] * dd[p]
+                H[dof + i * P + p, dof + i * P + p] += prior_alpha(prob, opts, i) * m[p]
+                g[dof + i * P + p] += prior_alpha(prob, opts, i) * m[p] * dd[p]
     keep = list(free_index(prob.fixed, calib)) + list(range(dof, nv))
     keep = np.array(keep)
     Hk = H[np.ix_(keep, keep)]

@@ -37,7 +37,7 @@ class ProblemDesc(ctypes.Structure):
         ("ii", ctypes.POINTER(c_i32)), ("jj", ctypes.POINTER(c_i32)),
         ("fixed", ctypes.POINTER(ctypes.c_uint8)),
         ("optimize_intrinsics", c_i32), ("use_prior", c_i32), ("scale_gauge", c_i32),
-        ("rank", c_i32), ("nranks", c_i32),
+        ("rank", c_i32), ("nranks", c_i32), ("freeze_disparities", c_i32),
     ]
 
 
@@ -54,7 +54,7 @@ class Buffers(ctypes.Structure):
         ("poses_in", c_vp), ("poses_out", c_vp), ("disps_in", c_vp), ("disps_out", c_vp),
         ("intr_in", c_vp), ("intr_out", c_vp), ("flow", c_vp), ("prior", c_vp),
         ("prior_mask", c_vp), ("workspace", c_vp), ("workspace_bytes", ctypes.c_size_t),
-        ("stream", c_vp), ("nccl_comm", c_vp),
+        ("stream", c_vp), ("nccl_comm", c_vp), ("prior_weight", c_vp),
     ]
 
 
@@ -89,6 +89,7 @@ EXPORTS = (
     "dba_plan_set_profiling", "dba_plan_get_stats", "dba_debug_trial", "dba_nccl_unique_id", "dba_nccl_comm_init", "dba_nccl_comm_destroy",
     "dba_dspt_read_flows", "dba_dspt_read_priors", "dba_dspt_load_flows",
     "dba_frame_distance", "dba_frontend_edges", "dba_backend_edges",
+    "dba_prior_affine", "dba_fit_affine",
 )
 
 _lib = None
@@ -163,6 +164,10 @@ def load():
     lib.dba_backend_edges.restype = c_i32
     lib.dba_backend_edges.argtypes = [c_i32, P(c_i32), P(c_dbl), c_i32, c_i32, c_i32, P(c_i32), P(c_i32),
                                       c_i32, P(c_i32), P(c_i32), P(c_i32)]
+    lib.dba_prior_affine.restype = c_i32
+    lib.dba_prior_affine.argtypes = [c_i32, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]
+    lib.dba_fit_affine.restype = c_i32
+    lib.dba_fit_affine.argtypes = [c_i32, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_dbl, c_vp]
     _lib = lib
     return lib
 

@@ -82,7 +82,7 @@ struct Layout {
 
 struct dba_plan {
   int N = 0, H = 0, W = 0, P = 0, E = 0;
-  int calib = 0, prior = 0, gauge_on = 0, gauge_frame = -1, rank = 0, nranks = 1;
+  int calib = 0, prior = 0, freeze_d = 0, gauge_on = 0, gauge_frame = -1, rank = 0, nranks = 1;
   int f0 = 0, f1 = 0, NL = 0, EL = 0, kmax = 0, nb = 0, BW = 0, n_red = 0;
   int n_tiles = 0, G = 0, nseg = 0, n_units = 0, nve = kEdgeVals, stage = 1;
   size_t pass_smem = 0, solve_smem = 0;
@@ -204,11 +204,13 @@ int dba_plan_create(const dba_problem_desc* d, dba_plan** out) {
   p->E = E;
   p->calib = d->optimize_intrinsics ? 1 : 0;
   p->prior = d->use_prior ? 1 : 0;
+  p->freeze_d = d->freeze_disparities ? 1 : 0;
   p->rank = d->rank;
   p->nranks = d->nranks;
   p->nve = kEdgeVals + (p->calib ? kCalibVals : 0);
   int gauge = d->scale_gauge;
-  if (gauge < 0) gauge = (nfixed == 1 && !p->prior) ? 1 : 0;
+  if (gauge < 0) gauge = (nfixed == 1 && !p->prior && !p->freeze_d) ? 1 : 0;
+  if (p->freeze_d) gauge = 0;  // the scale gauge acts on disparities
   p->gauge_on = gauge;
   for (int k = 0; k < N && p->gauge_frame < 0; ++k)
     if (d->fixed[k]) p->gauge_frame = k;
@@ -768,6 +770,8 @@ int launch_pass(Ctx& c, int cur, int nxt, bool backsub, bool system) {
   a.d_new = c.at<float>(p->L.disps[nxt]);
   a.prior = p->prior ? c.b->prior : nullptr;
   a.pmask = p->prior ? c.b->prior_mask : nullptr;
+  a.pweight = p->prior ? c.b->prior_weight : nullptr;
+  a.freeze = p->freeze_d;
   a.alpha = (float)c.o->alpha;
   a.eta = (float)c.o->eta;
   a.d_min = (float)c.o->d_min;

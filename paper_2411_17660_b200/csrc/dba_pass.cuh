@@ -46,6 +46,7 @@ constexpr int kEdgeSlots = 2;  // distinct edges per warp per segment (4k units 
 struct PassArgs {
   int H, W, P, n_tiles, kmax;
   int backsub;  // run phase A
+  int freeze;   // disparity block frozen (motion-only / pose stage): no Schur fill-in, d unchanged
   int system;   // produce system partials (0: energy only)
   int stage;    // flow records of the next sub-tile are staged in smem with cp.async
   const int* status;  // see trial_skipped
@@ -63,6 +64,7 @@ struct PassArgs {
   float* d_new;
   const float* prior;
   const uint8_t* pmask;
+  const float* pweight;  // (N,) per-frame multiplier of alpha (Eq. 5 stage A: s_i^2) or null
   float alpha, eta, d_min;
   const double* intr_c;
   const double* intr_n;
@@ -305,7 +307,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) pass_kernel(const PassArgs A)
       }
       __syncthreads();
       // ------------------------------------------------------------ phase A
-      if (A.backsub) {
+      if (A.backsub && !A.freeze) {
 #ifndef DBA_PASS_SKIP_A
         for (int u = u0; u < u1; ++u) {
           const int a = u / kSlices, sl0 = (u % kSlices) * kSlice;
@@ -357,7 +359,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) pass_kernel(const PassArgs A)
             const float dc = dcs[tid];
             if (A.prior != nullptr) {
               const size_t fp = (size_t)f * P + p;
-              const float ap = A.alpha * (float)A.pmask[fp];
+              const float ap = A.alpha * (A.pweight ? A.pweight[f] : 1.f) * (float)A.pmask[fp];
               C += ap;
               gd += ap * (A.prior[fp] - dc);
             }
@@ -504,7 +506,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) pass_kernel(const PassArgs A)
         const float dn = dns[tid];
         if (A.prior != nullptr && in) {
           const size_t fp = (size_t)f * P + p;
-          const float ap = A.alpha * (float)A.pmask[fp];
+          const float ap = A.alpha * (A.pweight ? A.pweight[f] : 1.f) * (float)A.pmask[fp];
           const float dd = A.prior[fp] - dn;
           C += ap;
           gd += ap * dd;
@@ -521,7 +523,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) pass_kernel(const PassArgs A)
             U2[1] = make_float2(Et[2], Et[3]);
           }
           // V = U_ext / sqrt(C): the GEMM below is then M_ext = V V^T
-          const float sq = in ? rsqrtf(C) : 0.f;
+          const float sq = (in && !A.freeze) ? rsqrtf(C) : 0.f;  // frozen d: no fill-in
           float2* U2 = reinterpret_cast<float2*>(Urow);
           for (int c = 0; c < (mu >> 1); ++c) {  // mu is even
             const float2 v = U2[c];

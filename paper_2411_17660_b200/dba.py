@@ -153,7 +153,7 @@ class DBASolver:
 
     def __init__(self, ii, jj, n_frames, height, width, fixed, *, optimize_intrinsics=False,
                  use_prior=False, scale_gauge=None, rank=0, nranks=1, device=None,
-                 nccl_comm=None):
+                 nccl_comm=None, freeze_disparities=False):
         self.lib = _lib.load()
         self.device = _device(device)
         self.ii = np.ascontiguousarray(ii, dtype=np.int32)
@@ -168,6 +168,7 @@ class DBASolver:
         self.n_frames, self.height, self.width = int(n_frames), int(height), int(width)
         self.optimize_intrinsics = bool(optimize_intrinsics)
         self.use_prior = bool(use_prior)
+        self.freeze_disparities = bool(freeze_disparities)
         self.rank, self.nranks = int(rank), int(nranks)
         self.nccl_comm = nccl_comm
         desc = _lib.ProblemDesc(
@@ -176,7 +177,8 @@ class DBASolver:
             self.jj.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
             self.fixed.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8)),
             int(self.optimize_intrinsics), int(self.use_prior),
-            -1 if scale_gauge is None else int(bool(scale_gauge)), self.rank, self.nranks)
+            -1 if scale_gauge is None else int(bool(scale_gauge)), self.rank, self.nranks,
+            int(self.freeze_disparities))
         handle = ctypes.c_void_p()
         with torch.cuda.device(self.device):
             code = self.lib.dba_plan_create(ctypes.byref(desc), ctypes.byref(handle))
@@ -212,7 +214,7 @@ class DBASolver:
         return _lib.Options(int(iters), o["lambda0"], o["lambda_min"], o["lambda_max"], o["eta"],
                             o["alpha"], o["d_min"], o["tangent_max"], o["calib_cond_max"])
 
-    def _inputs(self, poses, disps, intr, flow, prior, prior_mask):
+    def _inputs(self, poses, disps, intr, flow, prior, prior_mask, prior_weight=None):
         dev = self.device
         P = _to_dev(poses, torch.float64, dev)
         D = _to_dev(disps, torch.float32, dev)
@@ -232,6 +234,11 @@ class DBASolver:
             PR = _to_dev(prior, torch.float32, dev)
             PM = (_to_dev(prior_mask, torch.uint8, dev) if prior_mask is not None
                   else (PR > 0).to(torch.uint8))
+        self._pw = None
+        if prior_weight is not None:
+            self._pw = _to_dev(prior_weight, torch.float32, dev).reshape(-1)
+            if self._pw.shape != (N,):
+                raise ConfigError(f"prior_weight must be (N={N},)")
         return P, D, K, F, PR, PM
 
     def _buffers(self, P, D, K, F, PR, PM, Po=None, Do=None, Ko=None, stream=None):
@@ -242,13 +249,15 @@ class DBASolver:
             Ko.data_ptr() if Ko is not None else None, F.data_ptr(),
             PR.data_ptr() if PR is not None else None, PM.data_ptr() if PM is not None else None,
             self._ws_ptr, int(self.info.workspace_bytes), st.cuda_stream,
-            self.nccl_comm if self.nccl_comm is not None else None)
+            self.nccl_comm if self.nccl_comm is not None else None,
+            self._pw.data_ptr() if getattr(self, "_pw", None) is not None else None)
 
     def solve(self, poses, disps, intr, flow, prior=None, prior_mask=None, *, iters=4,
-              out=None, stream=None, **opts):
+              out=None, stream=None, prior_weight=None, **opts):
         """Damped Gauss-Newton.  Returns (poses', disps', intr', BAReport)
-        as device tensors.  ``out`` may supply preallocated (poses, disps, intr)."""
-        P, D, K, F, PR, PM = self._inputs(poses, disps, intr, flow, prior, prior_mask)
+        as device tensors.  ``out`` may supply preallocated (poses, disps, intr).
+        ``prior_weight`` (N,) scales alpha per frame (the Eq. 5 affine prior)."""
+        P, D, K, F, PR, PM = self._inputs(poses, disps, intr, flow, prior, prior_mask, prior_weight)
         if out is None:
             Po, Do, Ko = torch.empty_like(P), D.clone(), torch.empty_like(K)
         else:
@@ -268,8 +277,9 @@ class DBASolver:
             scale=rep.scale, calib_condition=rep.calib_condition)
         return Po, Do, Ko, report
 
-    def energy(self, poses, disps, intr, flow, prior=None, prior_mask=None, **opts):
-        P, D, K, F, PR, PM = self._inputs(poses, disps, intr, flow, prior, prior_mask)
+    def energy(self, poses, disps, intr, flow, prior=None, prior_mask=None, prior_weight=None,
+               **opts):
+        P, D, K, F, PR, PM = self._inputs(poses, disps, intr, flow, prior, prior_mask, prior_weight)
         buf = self._buffers(P, D, K, F, PR, PM)
         e = ctypes.c_double()
         o = self._options(0, **opts)
@@ -279,9 +289,10 @@ class DBASolver:
         _raise_for(code)
         return float(e.value)
 
-    def build_system(self, poses, disps, intr, flow, prior=None, prior_mask=None, **opts):
+    def build_system(self, poses, disps, intr, flow, prior=None, prior_mask=None, prior_weight=None,
+                     **opts):
         """(S, y, energy) of the Schur-reduced system at the given state (float64 host)."""
-        P, D, K, F, PR, PM = self._inputs(poses, disps, intr, flow, prior, prior_mask)
+        P, D, K, F, PR, PM = self._inputs(poses, disps, intr, flow, prior, prior_mask, prior_weight)
         buf = self._buffers(P, D, K, F, PR, PM)
         n = int(self.info.n_reduced)
         S = np.zeros((max(n, 1), max(n, 1)))

@@ -101,6 +101,36 @@ def exp_se3(xi):
     return pose_from_Rt(R, V @ v)
 
 
+def log_so3(R):
+    """Rotation vector of R (geometry.py:154-171, incl. the near-pi branch)."""
+    R = np.asarray(R, dtype=np.float64)
+    th = float(np.arccos(np.clip((np.trace(R) - 1.0) / 2.0, -1.0, 1.0)))
+    sk = np.array([R[2, 1] - R[1, 2], R[0, 2] - R[2, 0], R[1, 0] - R[0, 1]])
+    if th < 1e-8:
+        return sk / 2.0
+    if np.pi - th < 1e-6:
+        A = (R + np.eye(3)) / 2.0
+        ax = np.sqrt(np.maximum(np.diag(A), 0.0))
+        k = int(np.argmax(ax))
+        ax = A[:, k] / max(ax[k], 1e-12)
+        ax = ax / np.linalg.norm(ax)
+        return th * (ax if sk @ ax >= 0 else -ax)
+    return th / (2.0 * np.sin(th)) * sk
+
+
+def log_se3(p):
+    """se(3) logarithm (v, w) of a 7-vector pose (geometry.py:174-177)."""
+    w = log_so3(pose_rot(p))
+    th = float(np.linalg.norm(w))
+    W = np.array([[0, -w[2], w[1]], [w[2], 0, -w[0]], [-w[1], w[0], 0]])
+    if th < 1e-6:
+        Vinv = np.eye(3) - 0.5 * W + W @ W / 12.0
+    else:
+        Vinv = (np.eye(3) - 0.5 * W +
+                (1.0 / th**2) * (1.0 - th * np.sin(th) / (2.0 * (1.0 - np.cos(th)))) * (W @ W))
+    return np.concatenate([Vinv @ np.asarray(p[4:], np.float64), w])
+
+
 def project_points(pts, fx, fy, cx, cy, width, height, z_min=1e-4):
     """Pinhole projection + validity (closed bounds, eps 1e-9; geometry.py:235-250)."""
     z = pts[..., 2]

@@ -1,0 +1,204 @@
+"""P-RGBD block-coordinate descent and motion-only fill-in:
+oracle pins (SPEC.md:340-348, 358-366 examples) on CPU, GPU parity vs the oracle."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from oracle import dba as O
+from oracle import geometry as OG
+from oracle import prgbd as OB
+from paper_2411_17660_b200 import geometry as geo
+from paper_2411_17660_b200 import scenes
+
+REL = 1e-4
+
+
+def _scene(a=2.0, b=0.5, frames=8, radius=2, h=12, w=16, traj="orbit"):
+    spec = scenes.SceneSpec(trajectory=traj, frames=300 if traj == "orbit" else 40, height=h, width=w,
+                            seed=0, prior_scale_range=(a, a), prior_offset_range=(b, b))
+    sc = scenes.Scene(spec)
+    fr = list(range(frames))
+    ii, jj = scenes.radius_edges(frames, radius)
+    flow = np.stack([sc.flow_record(fr[x], fr[y]) for x, y in zip(ii, jj)])
+    poses0, disps0 = scenes.perturbed_state(sc, fr)
+    true_p = np.stack([sc.w2c[k] for k in fr])
+    true_d = np.stack([sc.disparity(k) for k in fr])
+    prior = np.stack([sc.depth_prior(k) for k in fr]).astype(np.float32)
+    mask = (prior > 0).astype(np.uint8)
+    fixed = np.zeros(frames, dtype=bool)
+    fixed[0] = True
+    return sc, ii, jj, flow, poses0, disps0.astype(np.float32), true_p, true_d, prior, mask, fixed
+
+
+# ----------------------------------------------------------------- oracle pins
+
+def test_oracle_affine_recovery_and_identity():
+    sc, ii, jj, flow, p0, d0, tp, td, prior, mask, fixed = _scene()
+    s, o = OB.fit_affine(td, prior, mask, np.ones(8), np.zeros(8))
+    assert np.allclose(s, 2.0, atol=1e-6) and np.allclose(o, 0.5, atol=1e-6)
+    s1, o1 = OB.fit_affine(td, td.astype(np.float32), mask, np.ones(8), np.zeros(8))
+    assert np.allclose(s1, 1.0, atol=1e-6) and np.allclose(o1, 0.0, atol=1e-6)
+    # clamp: a decreasing relation is forced to s = 1e-4 with the matching offset
+    s2, o2 = OB.fit_affine(td, (3.0 - td).astype(np.float32), mask, np.ones(8), np.zeros(8))
+    assert np.all(s2 == 1e-4)
+
+
+def test_oracle_bcd_monotone_and_fits_prior():
+    sc, ii, jj, flow, p0, d0, tp, td, prior, mask, fixed = _scene()
+    prob = O.Problem(ii, jj, flow, fixed)
+    st = O.State(p0.copy(), d0.astype(np.float64), sc.intr.copy())
+    out, s, o, trace = OB.solve_prgbd_bcd(st, prob, prior, mask, opts=O.Options(iters=4))
+    assert all(b <= a * (1 + 1e-12) for a, b in zip(trace, trace[1:])), trace
+    # mono: the global scale is free, so (s, o) fit the prior to the optimised
+    # disparities — the affine residual collapses
+    r0 = np.sqrt(np.mean((prior - d0) ** 2))
+    r1 = np.sqrt(np.mean((prior - (s[:, None, None] * out.disps + o[:, None, None])) ** 2))
+    assert r1 < 1e-2 * r0
+
+
+def test_oracle_bcd_identity_prior_fixpoint():
+    # prior equals the true disparity and the state starts at the truth: s -> 1, o -> 0
+    sc, ii, jj, flow, p0, d0, tp, td, prior, mask, fixed = _scene(a=1.0, b=0.0)
+    st = O.State(tp.copy(), td.astype(np.float64), sc.intr.copy())
+    out, s, o, trace = OB.solve_prgbd_bcd(st, O.Problem(ii, jj, flow, fixed), prior, mask)
+    assert np.allclose(s, 1.0, atol=1e-6) and np.allclose(o, 0.0, atol=1e-6)
+
+
+def test_oracle_freeze_is_pose_only():
+    sc, ii, jj, flow, p0, d0, tp, td, prior, mask, fixed = _scene()
+    prob = O.Problem(ii, jj, flow, fixed, freeze_disparities=True)
+    st = O.State(p0.copy(), td.astype(np.float64), sc.intr.copy())
+    out, rep = O.solve(st, prob, O.Options(iters=3))
+    assert np.array_equal(out.disps, st.disps)
+    assert rep.final_energy < rep.initial_energy
+    te = max(np.linalg.norm(a[4:] - b[4:]) / np.linalg.norm(b[4:]) for a, b in zip(out.poses[1:], tp[1:]))
+    assert te < 1e-3
+
+
+def _fill_setup():
+    spec = scenes.SceneSpec(trajectory="line", frames=40, height=12, width=16, seed=0)
+    sc = scenes.Scene(spec)
+    kf = [0, 3, 6, 9]
+    frames = list(range(10))
+    kp = np.stack([sc.w2c[k] for k in kf])
+    kd = np.stack([sc.disparity(k) for k in kf]).astype(np.float32)
+    flows = {}
+    for t in frames:
+        if t in kf:
+            continue
+        a, b = OB.bracket(kf, t)
+        for k in {a, b}:
+            flows[(k, t)] = sc.flow_record(k, t)
+    return sc, kf, frames, kp, kd, flows
+
+
+def test_oracle_fill_interpolation_and_refinement():
+    sc, kf, frames, kp, kd, flows = _fill_setup()
+    interp = OB.fill_nonkeyframe_poses(kf, kp, kd, sc.intr, frames, flows=None)
+    assert np.array_equal(interp[3], kp[1])  # coincides with a keyframe: identical
+    # provider disabled: on the geodesic, log(G_t G_a^-1) = tau log(G_b G_a^-1)
+    d_ab = OG.se3_log(OG.pose_compose(kp[1], OG.pose_inverse(kp[0])))
+    d_at = OG.se3_log(OG.pose_compose(interp[1], OG.pose_inverse(kp[0])))
+    assert np.allclose(d_at, d_ab / 3.0, atol=1e-12)
+    ref = OB.fill_nonkeyframe_poses(kf, kp, kd, sc.intr, frames, flows=flows, opts=O.Options(iters=6))
+    for t in frames:
+        assert np.linalg.norm(ref[t][4:] - sc.w2c[t][4:]) <= 1e-3 * max(np.linalg.norm(sc.w2c[t][4:]), 1.0)
+        assert OG.rotation_angle_deg(ref[t][:4], sc.w2c[t][:4]) < 1e-3
+
+
+def test_package_interpolate_matches_oracle():
+    from paper_2411_17660_b200.prgbd import interpolate
+    sc, kf, frames, kp, kd, flows = _fill_setup()
+    for tau in (0.0, 0.25, 0.5, 1.0):
+        assert np.allclose(interpolate(kp[0], kp[1], tau), OB.interpolate(kp[0], kp[1], tau), atol=1e-12)
+
+
+def test_package_log_se3_matches_reference(reference_flowsplat):
+    geometry, _ = reference_flowsplat
+    rng = np.random.default_rng(3)
+    for _ in range(8):
+        p = geo.exp_se3(rng.normal(size=6) * 0.8)
+        ref = geometry.se3_log(geometry.SE3Pose(p[:4], p[4:]))
+        assert np.allclose(geo.log_se3(p), ref, atol=1e-12)
+
+
+# ----------------------------------------------------------------- GPU parity
+
+@pytest.mark.gpu
+def test_gpu_fit_affine_and_prior_affine():
+    import torch
+
+    from paper_2411_17660_b200 import prgbd
+    sc, ii, jj, flow, p0, d0, tp, td, prior, mask, fixed = _scene()
+    D = torch.as_tensor(d0, device="cuda")
+    PR = torch.as_tensor(prior, device="cuda")
+    M = torch.as_tensor(mask, device="cuda")
+    s = torch.ones(8, dtype=torch.float64, device="cuda")
+    o = torch.zeros(8, dtype=torch.float64, device="cuda")
+    prgbd.fit_affine(D, PR, M, s, o)
+    se, oe = OB.fit_affine(d0, prior, mask, np.ones(8), np.zeros(8))
+    assert np.allclose(s.cpu().numpy(), se, rtol=1e-9) and np.allclose(o.cpu().numpy(), oe, rtol=1e-9, atol=1e-12)
+    eff, w = prgbd.affine_prior(PR, s, o)
+    exp = ((prior.astype(np.float64) - oe[:, None, None]) / se[:, None, None]).astype(np.float32)
+    assert np.allclose(eff.cpu().numpy(), exp, rtol=1e-6) and np.allclose(w.cpu().numpy(), se ** 2, rtol=1e-6)
+
+
+@pytest.mark.gpu
+def test_gpu_freeze_and_prior_weight_parity():
+    from paper_2411_17660_b200 import dba
+    from tests.helpers import pose_errors
+    sc, ii, jj, flow, p0, d0, tp, td, prior, mask, fixed = _scene()
+    # motion-only: poses vs the oracle, disparities untouched bit for bit
+    s = dba.DBASolver(ii, jj, 8, 12, 16, fixed, freeze_disparities=True)
+    Po, Do, _, rep = s.solve(p0, td.astype(np.float32), sc.intr, flow, iters=3)
+    ref, rrep = O.solve(O.State(p0.copy(), td.astype(np.float32).astype(np.float64), sc.intr.copy()),
+                        O.Problem(ii, jj, flow, fixed, freeze_disparities=True), O.Options(iters=3))
+    assert np.array_equal(Do.cpu().numpy(), td.astype(np.float32))
+    te, ae = pose_errors(Po.cpu().numpy(), ref.poses)
+    assert te < REL and ae < 1e-3 and rep.iterations_run == rrep.iterations
+    # per-frame prior weights in the reduced system
+    wts = np.linspace(0.5, 3.0, 8)
+    s2 = dba.DBASolver(ii, jj, 8, 12, 16, fixed, use_prior=True)
+    S, y, e = s2.build_system(p0, d0, sc.intr, flow, prior, mask, prior_weight=wts.astype(np.float32))
+    prob = O.Problem(ii, jj, flow, fixed, prior=prior, prior_mask=mask, prior_weight=wts.astype(np.float32))
+    sysm = O.linearize(O.State(p0.copy(), d0.astype(np.float64), sc.intr.copy()), prob, O.Options())
+    Sr, yr, _ = O.reduced(sysm, prob, O.Options())
+    assert np.linalg.norm(S - Sr) / np.linalg.norm(Sr) < REL
+    assert np.linalg.norm(y - yr) / np.linalg.norm(yr) < REL
+    assert abs(e - sysm.energy) < REL * sysm.energy
+
+
+@pytest.mark.gpu
+def test_gpu_bcd_parity():
+    from paper_2411_17660_b200 import prgbd
+    from tests.helpers import pose_errors
+    sc, ii, jj, flow, p0, d0, tp, td, prior, mask, fixed = _scene()
+    P, D, s, o, trace = prgbd.solve_prgbd_bcd(ii, jj, p0, d0, sc.intr, flow, prior, mask, fixed, iters=4)
+    st = O.State(p0.copy(), d0.astype(np.float64), sc.intr.copy())
+    ref, rs, ro, rtrace = OB.solve_prgbd_bcd(st, O.Problem(ii, jj, flow, fixed), prior, mask,
+                                             opts=O.Options(iters=4))
+    assert all(b <= a * (1 + 1e-6) for a, b in zip(trace, trace[1:])), trace
+    te, ae = pose_errors(P.cpu().numpy(), ref.poses)
+    assert te < REL and ae < 1e-3
+    rel = np.abs(D.cpu().numpy() - ref.disps) / ref.disps
+    assert rel.max() < 10 * REL and np.quantile(rel, 0.999) < REL
+    assert np.allclose(s.cpu().numpy(), rs, rtol=REL) and np.allclose(o.cpu().numpy(), ro, atol=REL)
+    # both blocks frozen: a no-op
+    P2, D2, *_ = prgbd.solve_prgbd_bcd(ii, jj, p0, d0, sc.intr, flow, prior, mask, fixed,
+                                       freeze_poses=True, freeze_structure=True)
+    assert np.array_equal(P2.cpu().numpy(), p0) and np.array_equal(D2.cpu().numpy(), d0)
+
+
+@pytest.mark.gpu
+def test_gpu_fill_nonkeyframe_parity():
+    from paper_2411_17660_b200 import prgbd
+    sc, kf, frames, kp, kd, flows = _fill_setup()
+    got = prgbd.fill_nonkeyframe_poses(kf, kp, kd, sc.intr, frames, flows=flows, iters=6)
+    ref = OB.fill_nonkeyframe_poses(kf, kp, kd, sc.intr, frames, flows=flows, opts=O.Options(iters=6))
+    for t in frames:
+        n = max(np.linalg.norm(ref[t][4:]), 1e-12)
+        assert np.linalg.norm(got[t][4:] - ref[t][4:]) / n < REL
+        assert OG.rotation_angle_deg(got[t][:4], ref[t][:4]) < 1e-3
+        assert np.linalg.norm(got[t][4:] - sc.w2c[t][4:]) <= 1e-3 * max(np.linalg.norm(sc.w2c[t][4:]), 1.0)
