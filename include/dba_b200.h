@@ -261,6 +261,16 @@ int dba_prior_affine(int32_t n_frames, int32_t n_pixels, const float* prior, con
 int dba_fit_affine(int32_t n_frames, int32_t n_pixels, const float* disps, const float* prior, const uint8_t* mask,
                    double* scale, double* offset, double s_min, void* stream);
 
+/* GPU synthetic correspondence provider: flow records of
+ * SyntheticProviders.provide_correspondences (providers.py:318-338) for n_edges
+ * edges (ii[e] -> jj[e]) of the analytic scene (outer sphere of outer_radius,
+ * spherical occluders (n,4) [centre, radius], camera poses c2w / w2c (F,7)),
+ * one thread per edge-pixel, float64, into out (E,H,W,4) float32.  intr is a
+ * HOST (4,) array; every other pointer is DEVICE.  Pixel noise is not added. */
+int dba_synthetic_flows(int32_t H, int32_t W, const double* intr, double outer_radius, int32_t n_occluders,
+                        const double* occluders, const double* c2w, const double* w2c, int32_t n_edges,
+                        const int32_t* ii, const int32_t* jj, float* out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

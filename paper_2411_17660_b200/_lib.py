@@ -89,7 +89,7 @@ EXPORTS = (
     "dba_plan_set_profiling", "dba_plan_get_stats", "dba_debug_trial", "dba_nccl_unique_id", "dba_nccl_comm_init", "dba_nccl_comm_destroy",
     "dba_dspt_read_flows", "dba_dspt_read_priors", "dba_dspt_load_flows",
     "dba_frame_distance", "dba_frontend_edges", "dba_backend_edges",
-    "dba_prior_affine", "dba_fit_affine",
+    "dba_prior_affine", "dba_fit_affine", "dba_synthetic_flows",
 )
 
 _lib = None
@@ -168,6 +168,9 @@ def load():
     lib.dba_prior_affine.argtypes = [c_i32, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]
     lib.dba_fit_affine.restype = c_i32
     lib.dba_fit_affine.argtypes = [c_i32, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_dbl, c_vp]
+    lib.dba_synthetic_flows.restype = c_i32
+    lib.dba_synthetic_flows.argtypes = [c_i32, c_i32, P(c_dbl), c_dbl, c_i32, c_vp, c_vp, c_vp, c_i32, c_vp,
+                                        c_vp, c_vp, c_vp]
     _lib = lib
     return lib
 

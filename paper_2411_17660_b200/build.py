@@ -37,7 +37,8 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         return OUT
     cmd = [nvcc_path(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
            "-shared", "-o", str(OUT) + ".tmp", str(SRC / "dba_host.cu"), str(SRC / "dba_ingest.cu"),
-           str(SRC / "dba_graph.cu"), str(SRC / "dba_prgbd.cu"), "-ldl"]
+           str(SRC / "dba_graph.cu"), str(SRC / "dba_prgbd.cu"),
+           str(SRC / "dba_provider.cu"), "-ldl"]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd), file=sys.stderr)
