@@ -718,7 +718,7 @@ int launch_prep(Ctx& c, int cur, int nxt, bool init) {
   a.back = c.at<EdgeBack>(p->L.back);
   a.adj = c.at<double>(p->L.adj);
   const int n = p->N + p->EL + 1;
-  prep_kernel<<<(n + 127) / 128, 128, 0, c.st>>>(a);
+  prep_kernel<<<(n + 31) / 32, 32, 0, c.st>>>(a);  // one warp per block: spread the fp64 work over SMs
   p->prof.launches++;
   return cuda_status(cudaGetLastError());
 }
@@ -790,7 +790,27 @@ int launch_pass(Ctx& c, int cur, int nxt, bool backsub, bool system) {
   return launch_pass_t<false>(c, a);
 }
 
-int launch_system(Ctx& c, int slot) {
+// LM controller inputs: the trial (slot 1) energy, the flags word and the options
+DecideArgs decide_args(Ctx& c) {
+  dba_plan* p = c.p;
+  DecideArgs a;
+  a.iters = c.o->iters;
+  a.calib = p->calib;
+  a.lam_min = c.o->lambda_min;
+  a.lam_max = c.o->lambda_max;
+  a.cond_max = c.o->calib_cond_max;
+  a.status = c.at<int>(p->L.flags);
+  a.cond = &c.at<Readback>(p->L.flags)->cond;
+  a.energy = c.at<double>(p->L.sys[1]) + p->energy_off;
+  a.ctl = c.at<Control>(p->L.ctl);
+  return a;
+}
+
+int launch_decide(Ctx& c);
+
+// assemble -> gather -> finalize [-> all-reduce]; with `decide` the LM decision on
+// the resulting trial energy follows (fused into finalize on a single rank)
+int launch_system(Ctx& c, int slot, bool decide = false) {
   dba_plan* p = c.p;
   if (p->NL > 0) {
     AsmArgs a;
@@ -815,7 +835,9 @@ int launch_system(Ctx& c, int slot) {
     a.gauge_frame = p->gauge_on ? p->gauge_frame : -1;
     a.frame_of = c.at<int>(p->L.frame_of);
     a.gstate = c.at<double>(p->L.gstate[slot]);
-    assemble_kernel<<<p->NL, 256, 0, c.st>>>(a);
+    const size_t smem = assemble_smem_bytes(std::max(p->kmax, 1), p->calib);
+    DBA_CUDA(cudaFuncSetAttribute(assemble_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    assemble_kernel<<<p->NL, 256, smem, c.st>>>(a);
     p->prof.launches++;
     DBA_CUDA(cudaGetLastError());
   }
@@ -837,10 +859,16 @@ int launch_system(Ctx& c, int slot) {
   f.status = c.at<int>(p->L.flags);
   f.part_frame = c.at<double>(p->L.part_frame);
   f.energy_out = c.at<double>(p->L.sys[slot]) + p->energy_off;
+  const bool multi = c.comm && p->nranks > 1;
+  if (decide && !multi) {
+    finalize_decide_kernel<<<1, 256, 0, c.st>>>(f, decide_args(c));
+    p->prof.launches++;
+    return cuda_status(cudaGetLastError());
+  }
   finalize_kernel<<<1, 256, 0, c.st>>>(f);
   p->prof.launches++;
   DBA_CUDA(cudaGetLastError());
-  if (c.comm && p->nranks > 1) {
+  if (multi) {
     if (!nccl().ok) return DBA_ENCCL;
     double* s = c.at<double>(p->L.sys[slot]);
     if (nccl().AllReduce(s, s, (size_t)p->sys_len, ncclDouble, ncclSum, c.comm, c.st) != ncclSuccess)
@@ -848,6 +876,7 @@ int launch_system(Ctx& c, int slot) {
     int* bad = c.at<int>(p->L.flags) + 1;
     if (nccl().AllReduce(bad, bad, 1, ncclInt32, ncclMin, c.comm, c.st) != ncclSuccess) return DBA_ENCCL;
   }
+  if (decide) return launch_decide(c);
   return DBA_OK;
 }
 
@@ -901,17 +930,7 @@ int launch_solve(Ctx& c, int slot) {
 
 int launch_decide(Ctx& c) {
   dba_plan* p = c.p;
-  DecideArgs a;
-  a.iters = c.o->iters;
-  a.calib = p->calib;
-  a.lam_min = c.o->lambda_min;
-  a.lam_max = c.o->lambda_max;
-  a.cond_max = c.o->calib_cond_max;
-  a.status = c.at<int>(p->L.flags);
-  a.cond = &c.at<Readback>(p->L.flags)->cond;
-  a.energy = c.at<double>(p->L.sys[1]) + p->energy_off;
-  a.ctl = c.at<Control>(p->L.ctl);
-  decide_kernel<<<1, 32, 0, c.st>>>(a);
+  decide_kernel<<<1, 32, 0, c.st>>>(decide_args(c));
   p->prof.launches++;
   return cuda_status(cudaGetLastError());
 }
@@ -931,7 +950,7 @@ int launch_accept(Ctx& c) {
        (long long)p->NL * p->P);
   span(p->L.sys[0], p->L.sys[1], 2 * p->sys_len);
   span(p->L.gstate[0], p->L.gstate[1], 2LL * (6 * kMaxOutDegree + 8));
-  accept_kernel<<<2 * std::max(p->G, 1), 256, 0, c.st>>>(a);
+  accept_kernel<<<dim3(std::max(p->G / 2, 1), a.nspan), 256, 0, c.st>>>(a);
   p->prof.launches++;
   return cuda_status(cudaGetLastError());
 }
@@ -1042,8 +1061,7 @@ int dba_solve(dba_plan* p, const dba_options* o, const dba_buffers* b, dba_repor
       if ((s = launch_solve(c, 0))) return rep->status = s;
       if ((s = launch_prep(c, 0, 1, false))) return rep->status = s;
       if ((s = launch_pass(c, 0, 1, true, true))) return rep->status = s;
-      if ((s = launch_system(c, 1))) return rep->status = s;
-      if ((s = launch_decide(c))) return rep->status = s;
+      if ((s = launch_system(c, 1, true))) return rep->status = s;
       if ((s = launch_accept(c))) return rep->status = s;
     }
     DBA_CUDA(cudaMemcpyAsync(p->ctl_h, c.at<Control>(p->L.ctl), sizeof(Control), cudaMemcpyDeviceToHost, c.st));

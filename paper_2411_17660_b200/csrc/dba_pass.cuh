@@ -39,7 +39,7 @@ namespace dba {
 constexpr int kPassThreads = 512;
 constexpr int kPassWarps = 16;
 constexpr int kSub = 256;    // pixels per sub-tile
-constexpr int kSlice = 64;   // pixels per edge unit (2 per lane)
+constexpr int kSlice = 32;   // pixels per phase-B edge unit (1 per lane)
 constexpr int kSlices = kSub / kSlice;
 constexpr int kEdgeSlots = 2;  // distinct edges per warp per segment (4k units / 16 warps)
 
@@ -116,7 +116,7 @@ __host__ __device__ inline PassSmem pass_smem_layout(int kmax, bool calib, bool 
   PassSmem s;
   size_t o = 0;
   s.fbuf = o; o += stage ? sizeof(float4) * (size_t)kmax * kSub : 0;
-  const int nparts = calib ? 6 : 3;  // phase A: C, gd, acc ; phase B: C, gd (+ E_theta x4)
+  const int nparts = calib ? 6 : 2;  // phase B: C, gd (+ E_theta x4)
   s.ethb = o; o += calib ? sizeof(double) * kPassWarps * kEdgeSlots * 32 : 0;
   s.red = o; o += sizeof(double) * kPassWarps * 16;
   s.U = o; o += sizeof(float) * (size_t)kSub * pass_ustride(kmax, calib);
@@ -210,7 +210,6 @@ __global__ void __launch_bounds__(kPassThreads, 1) pass_kernel(const PassArgs A)
     const int ustride = mpad + 2;
     float* Pa0 = parts;                  // [k][kSub]  C part
     float* Pa1 = parts + KM * kSub;      // [k][kSub]  g_d part
-    float* Pa2 = parts + 2 * KM * kSub;  // [k][kSub]  back-substitution part (phase A)
     float* Pth = parts + 2 * KM * kSub;  // [4][k][kSub] E_theta parts (phase B, calib)
 
     // ---- stage per-edge constants, unit -> edge slots
@@ -307,56 +306,50 @@ __global__ void __launch_bounds__(kPassThreads, 1) pass_kernel(const PassArgs A)
       }
       __syncthreads();
       // ------------------------------------------------------------ phase A
+      // pixel-major: a half-warp per 16 pixels, the two halves split the edges; the
+      // per-pixel sums close with one shuffle, so d_n needs no block barrier
       if (A.backsub && !A.freeze) {
+        const int pl = 16 * warp + (lane & 15), p = pbase + pl, eg = lane >> 4;
+        const bool in = p < P;
+        const float dc = dcs[pl];
+        const float2 q = qcs[pl];
+        const float qx = q.x, qy = q.y;
+        float Cp = 0.f, gdp = 0.f, accp = 0.f;
 #ifndef DBA_PASS_SKIP_A
-        for (int u = u0; u < u1; ++u) {
-          const int a = u / kSlices, sl0 = (u % kSlices) * kSlice;
+        for (int a = eg; a < k; a += 2) {
           const EdgeBack& e = sb[a];
-          const float4* fl4 = A.flow + (size_t)sflow[a] * P;
-#pragma unroll
-          for (int i = 0; i < 2; ++i) {
-            const int pl = sl0 + lane + 32 * i, p = pbase + pl;
-            const bool in = p < P;
-            const float4 fw = A.stage ? fbuf[a * kSub + pl]
-                                      : (in ? __ldg(fl4 + p) : make_float4(0.f, 0.f, 0.f, 0.f));
-            const float dc = dcs[pl];
-            const float2 q = qcs[pl];
-            const float qx = q.x, qy = q.y;
-            const PixTerms T = pix_terms(e.R, e.t, qx, qy, dc, fxc, fyc, cxc, cyc, Wf, Hf, fw, in);
-            const float fxi = fxc * T.iz, fyi = fyc * T.iz;
-            const float Jdu = fxi * (e.t[0] - T.xt * e.t[2]);
-            const float Jdv = fyi * (e.t[1] - T.yt * e.t[2]);
-            const float* dl = e.dlt;
-            float ju = fxi * dc * (dl[0] - T.xt * dl[2]) +
-                       fxc * (-T.xt * T.yt * dl[3] + (1.f + T.xt * T.xt) * dl[4] - T.yt * dl[5]);
-            float jv = fyi * dc * (dl[1] - T.yt * dl[2]) +
-                       fyc * (-(1.f + T.yt * T.yt) * dl[3] + T.xt * T.yt * dl[4] + T.xt * dl[5]);
-            if (CALIB) {
-              const float cu0 = T.iz * (e.R[0] - T.xt * e.R[6]), cu1 = T.iz * (e.R[1] - T.xt * e.R[7]);
-              const float cv0 = T.iz * (e.R[3] - T.yt * e.R[6]), cv1 = T.iz * (e.R[4] - T.yt * e.R[7]);
-              ju += (T.xt - cu0 * qx) * dth[0] + (-cu1 * qy * fxc / fyc) * dth[1] + (1.f - cu0) * dth[2] +
-                    (-cu1 * fxc / fyc) * dth[3];
-              jv += (-cv0 * qx * fyc / fxc) * dth[0] + (T.yt - cv1 * qy) * dth[1] +
-                    (-cv0 * fyc / fxc) * dth[2] + (1.f - cv1) * dth[3];
-            }
-            const float au = T.wu * Jdu, av = T.wv * Jdv;
-            Pa0[a * kSub + pl] = fmaf(au, Jdu, av * Jdv);
-            Pa1[a * kSub + pl] = fmaf(au, T.ru, av * T.rv);
-            Pa2[a * kSub + pl] = fmaf(au, ju, av * jv);
+          const float4 fw = A.stage ? fbuf[a * kSub + pl]
+                                    : (in ? __ldg(A.flow + (size_t)sflow[a] * P + p) : make_float4(0.f, 0.f, 0.f, 0.f));
+          const PixTerms T = pix_terms(e.R, e.t, qx, qy, dc, fxc, fyc, cxc, cyc, Wf, Hf, fw, in);
+          const float fxi = fxc * T.iz, fyi = fyc * T.iz;
+          const float Jdu = fxi * (e.t[0] - T.xt * e.t[2]);
+          const float Jdv = fyi * (e.t[1] - T.yt * e.t[2]);
+          const float* dl = e.dlt;
+          float ju = fxi * dc * (dl[0] - T.xt * dl[2]) +
+                     fxc * (-T.xt * T.yt * dl[3] + (1.f + T.xt * T.xt) * dl[4] - T.yt * dl[5]);
+          float jv = fyi * dc * (dl[1] - T.yt * dl[2]) +
+                     fyc * (-(1.f + T.yt * T.yt) * dl[3] + T.xt * T.yt * dl[4] + T.xt * dl[5]);
+          if (CALIB) {
+            const float cu0 = T.iz * (e.R[0] - T.xt * e.R[6]), cu1 = T.iz * (e.R[1] - T.xt * e.R[7]);
+            const float cv0 = T.iz * (e.R[3] - T.yt * e.R[6]), cv1 = T.iz * (e.R[4] - T.yt * e.R[7]);
+            ju += (T.xt - cu0 * qx) * dth[0] + (-cu1 * qy * fxc / fyc) * dth[1] + (1.f - cu0) * dth[2] +
+                  (-cu1 * fxc / fyc) * dth[3];
+            jv += (-cv0 * qx * fyc / fxc) * dth[0] + (T.yt - cv1 * qy) * dth[1] +
+                  (-cv0 * fyc / fxc) * dth[2] + (1.f - cv1) * dth[3];
           }
+          const float au = T.wu * Jdu, av = T.wv * Jdv;
+          Cp += fmaf(au, Jdu, av * Jdv);
+          gdp += fmaf(au, T.ru, av * T.rv);
+          accp += fmaf(au, ju, av * jv);
         }
 #endif
-        __syncthreads();
-        if (tid < kSub) {
-          const int p = pbase + tid;
-          if (p < P) {
-            float C = A.eta, gd = 0.f, acc = 0.f;
-            for (int a = 0; a < k; ++a) {
-              C += Pa0[a * kSub + tid];
-              gd += Pa1[a * kSub + tid];
-              acc += Pa2[a * kSub + tid];
-            }
-            const float dc = dcs[tid];
+        // edge-group halves in fixed order: (even edges) + (odd edges)
+        const float Co = __shfl_xor_sync(0xffffffffu, Cp, 16);
+        const float go = __shfl_xor_sync(0xffffffffu, gdp, 16);
+        const float ao = __shfl_xor_sync(0xffffffffu, accp, 16);
+        if (eg == 0) {
+          if (in) {
+            float C = A.eta + (Cp + Co), gd = gdp + go, acc = accp + ao;
             if (A.prior != nullptr) {
               const size_t fp = (size_t)f * P + p;
               const float ap = A.alpha * (A.pweight ? A.pweight[f] : 1.f) * (float)A.pmask[fp];
@@ -366,10 +359,10 @@ __global__ void __launch_bounds__(kPassThreads, 1) pass_kernel(const PassArgs A)
             float dd = (gd - acc) / C;
             if (gauge) dd -= (float)(kappa / (double)dc);  // A5: r/C - kappa/d
             const float dn = fmaxf(dc + dd, A.d_min);
-            dns[tid] = dn;
+            dns[pl] = dn;
             A.d_new[(size_t)f * P + p] = dn;
           } else {
-            dns[tid] = 1.f;
+            dns[pl] = 1.f;
           }
         }
       } else if (tid < kSub) {
@@ -386,6 +379,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) pass_kernel(const PassArgs A)
 #endif
         const int a = u / kSlices, sl0 = (u % kSlices) * kSlice;
         const int slot = a - e0;
+        (void)sl0;
         const EdgeLin& e = sl[a];
         const float4* fl4 = A.flow + (size_t)sflow[a] * P;
         float ct[24];
@@ -393,9 +387,8 @@ __global__ void __launch_bounds__(kPassThreads, 1) pass_kernel(const PassArgs A)
 #pragma unroll
           for (int x = 0; x < 24; ++x) ct[x] = 0.f;
         }
-#pragma unroll
-        for (int i = 0; i < 2; ++i) {
-          const int pl = sl0 + lane + 32 * i, p = pbase + pl;
+        {
+          const int pl = sl0 + lane, p = pbase + pl;
           const bool in = p < P;
           const float4 fw = A.stage ? fbuf[a * kSub + pl]
                                     : (in ? __ldg(fl4 + p) : make_float4(0.f, 0.f, 0.f, 0.f));
@@ -492,45 +485,50 @@ __global__ void __launch_bounds__(kPassThreads, 1) pass_kernel(const PassArgs A)
       __syncthreads();
       if (A.stage && tile + 1 < A.seg_t1[sg]) prefetch(tile + 1);  // overlaps the GEMM
       // ------------------------------------------------------------ per pixel
-      if (tid < kSub) {
-        const int p = pbase + tid;
+      // two threads per pixel: both form C_p, g_d,p; each scales half of the row
+      {
+        const int pl = tid & (kSub - 1), half = tid >> 8;
+        const int p = pbase + pl;
         const bool in = p < P;
-        float* Urow = U + tid * ustride;
+        float* Urow = U + pl * ustride;
         float C = A.eta, gd = 0.f;
         if (A.system) {
           for (int a = 0; a < k; ++a) {
-            C += Pa0[a * kSub + tid];
-            gd += Pa1[a * kSub + tid];
+            C += Pa0[a * kSub + pl];
+            gd += Pa1[a * kSub + pl];
           }
         }
-        const float dn = dns[tid];
+        const float dn = dns[pl];
         if (A.prior != nullptr && in) {
           const size_t fp = (size_t)f * P + p;
           const float ap = A.alpha * (A.pweight ? A.pweight[f] : 1.f) * (float)A.pmask[fp];
           const float dd = A.prior[fp] - dn;
           C += ap;
           gd += ap * dd;
-          facc[0] += ap * dd * dd;
+          if (half == 0) facc[0] += ap * dd * dd;
         }
         if (A.system) {
-          if (CALIB) {
-            float Et[4] = {0.f, 0.f, 0.f, 0.f};
-            for (int a = 0; a < k; ++a)
-#pragma unroll
-              for (int r = 0; r < 4; ++r) Et[r] += Pth[(r * KM + a) * kSub + tid];
-            float2* U2 = reinterpret_cast<float2*>(Urow + 6 * k);
-            U2[0] = make_float2(Et[0], Et[1]);
-            U2[1] = make_float2(Et[2], Et[3]);
-          }
           // V = U_ext / sqrt(C): the GEMM below is then M_ext = V V^T
           const float sq = (in && !A.freeze) ? rsqrtf(C) : 0.f;  // frozen d: no fill-in
           float2* U2 = reinterpret_cast<float2*>(Urow);
-          for (int c = 0; c < (mu >> 1); ++c) {  // mu is even
+          const int ne = 3 * k;  // float2 columns of the edge rows
+          const int c0 = half ? ne / 2 : 0, c1 = half ? ne : ne / 2;
+          for (int c = c0; c < c1; ++c) {
             const float2 v = U2[c];
             U2[c] = make_float2(v.x * sq, v.y * sq);
           }
-          U2[mu >> 1] = make_float2(gd * sq, in ? C / dn * sq : 0.f);  // A5 with c = C/d
-          for (int c = (mext >> 1); c < (mpad >> 1); ++c) U2[c] = make_float2(0.f, 0.f);
+          if (half) {
+            if (CALIB) {
+              float Et[4] = {0.f, 0.f, 0.f, 0.f};
+              for (int a = 0; a < k; ++a)
+#pragma unroll
+                for (int r = 0; r < 4; ++r) Et[r] += Pth[(r * KM + a) * kSub + pl];
+              U2[ne] = make_float2(Et[0] * sq, Et[1] * sq);
+              U2[ne + 1] = make_float2(Et[2] * sq, Et[3] * sq);
+            }
+            U2[mu >> 1] = make_float2(gd * sq, in ? C / dn * sq : 0.f);  // A5 with c = C/d
+            for (int c = (mext >> 1); c < (mpad >> 1); ++c) U2[c] = make_float2(0.f, 0.f);
+          }
         }
       }
       __syncthreads();

@@ -154,8 +154,15 @@ __device__ __forceinline__ int tri4(int r, int c) {
   return r * 4 - r * (r - 1) / 2 + (c - r);
 }
 
+// dynamic shared memory of assemble_kernel: the frame's M (mu x mu float64)
+__host__ __device__ inline size_t assemble_smem_bytes(int kmax, bool calib) {
+  const size_t mu = 6 * (size_t)kmax + (calib ? 4 : 0);
+  return sizeof(double) * mu * mu;
+}
+
 __global__ void __launch_bounds__(256) assemble_kernel(const AsmArgs A) {
   if (trial_skipped(A.status)) return;
+  extern __shared__ double Ms[];  // M = sum_p v_p v_p^T / C_p over u-space (mu x mu)
   __shared__ double Ad[kMaxOutDegree * 36];
   __shared__ double hs[kMaxOutDegree * (kEdgeVals + kCalibVals)];
   __shared__ double ws[6 * kMaxOutDegree + 4];
@@ -163,6 +170,8 @@ __global__ void __launch_bounds__(256) assemble_kernel(const AsmArgs A) {
   __shared__ double Nm[6 * (6 * kMaxOutDegree + 4)];
   __shared__ double hg[6 * kMaxOutDegree + 4];
   __shared__ double Th[6 * kMaxOutDegree + 10];
+  __shared__ double Tb[kMaxOutDegree * 36];  // per-edge Ad_e^T H_e
+  __shared__ double Tc[kMaxOutDegree * 36];  // per-edge pose-block terms
   const int fl = blockIdx.x, tid = threadIdx.x;
   const int s0 = A.csr_off[fl], k = A.csr_off[fl + 1] - s0;
   if (k == 0) return;
@@ -172,32 +181,28 @@ __global__ void __launch_bounds__(256) assemble_kernel(const AsmArgs A) {
   double* fv = A.Fbuf + A.off_f[fl];
   const int sg0 = A.frame_seg[fl], sg1 = A.frame_seg[fl + 1];
 
+  // segment partials, summed in segment order; each pass over x issues its loads
+  // independently (unrolled) so the loop is bandwidth-, not latency-bound
   for (int x = tid; x < k * 36; x += blockDim.x) Ad[x] = A.adj[36 * (size_t)s0 + x];
-  for (int x = tid; x < k * nve; x += blockDim.x) {
-    double s = 0.0;
-    for (int sg = sg0; sg < sg1; ++sg) s += A.part_edge[A.seg_off_edge[sg] + x];
-    hs[x] = s;
-  }
   const bool gauge = A.frame_of[fl] == A.gauge_frame;
-  for (int x = tid; x < mu; x += blockDim.x) {
-    double s = 0.0, h = 0.0;
-    for (int sg = sg0; sg < sg1; ++sg) {
-      s += A.part_w[A.seg_off_w[sg] + x];
-      h += A.part_w[A.seg_off_w[sg] + mu + x];
+  for (int sg = sg0; sg < sg1; ++sg) {
+    const bool first = sg == sg0;
+    const double* pe = A.part_edge + A.seg_off_edge[sg];
+    const double* pw = A.part_w + A.seg_off_w[sg];
+    const double* pm = A.part_M + A.seg_off_M[sg];
+#pragma unroll 4
+    for (int x = tid; x < k * nve; x += blockDim.x) hs[x] = first ? pe[x] : hs[x] + pe[x];
+#pragma unroll 2
+    for (int x = tid; x < mu; x += blockDim.x) {
+      ws[x] = first ? pw[x] : ws[x] + pw[x];
+      hg[x] = first ? pw[mu + x] : hg[x] + pw[mu + x];
     }
-    ws[x] = s;
-    hg[x] = h;
-  }
-  if (tid < kFrameVals) {
-    double s = 0.0;
-    for (int sg = sg0; sg < sg1; ++sg) s += A.part_frame[(long long)sg * kFrameVals + tid];
-    fs[tid] = s;
-  }
-  for (int x = tid; x < mu * mu; x += blockDim.x) {
-    double s = 0.0;
-    for (int sg = sg0; sg < sg1; ++sg) s += A.part_M[A.seg_off_M[sg] + x];
-    const int r = x / mu, c = x % mu;
-    F[(long long)(6 + r) * m + 6 + c] = -s;
+    if (tid < kFrameVals) {
+      const double v = A.part_frame[(long long)sg * kFrameVals + tid];
+      fs[tid] = first ? v : fs[tid] + v;
+    }
+#pragma unroll 8
+    for (int x = tid; x < mu * mu; x += blockDim.x) Ms[x] = first ? pm[x] : Ms[x] + pm[x];
   }
   __syncthreads();
   if (tid < k) {
@@ -205,18 +210,37 @@ __global__ void __launch_bounds__(256) assemble_kernel(const AsmArgs A) {
     for (int x = 0; x < nve; ++x) ok = ok && isfinite(hs[tid * nve + x]);
     if (!ok) atomicMin(A.bad_edge, A.slot_edge[s0 + tid]);
   }
-  // N = sum_e Ad_e^T M[e, :]   (6 x mu); F currently holds -M in the u x u block
+  // N = sum_e Ad_e^T M[e, :]   (6 x mu)
   for (int x = tid; x < 6 * mu; x += blockDim.x) {
     const int r = x / mu, c = x % mu;
     double s = 0.0;
     for (int e = 0; e < k; ++e)
-      for (int q = 0; q < 6; ++q) s -= Ad[36 * e + 6 * q + r] * F[(long long)(6 + 6 * e + q) * m + 6 + c];
+      for (int q = 0; q < 6; ++q) s += Ad[36 * e + 6 * q + r] * Ms[(6 * e + q) * mu + c];
     Nm[x] = s;
+  }
+  // (Ad_e^T H_e) per edge, 6x6 each
+  for (int x = tid; x < k * 36; x += blockDim.x) {
+    const int e = x / 36, r = (x / 6) % 6, q = x % 6;
+    const double* Ae = Ad + 36 * e;
+    const double* He = hs + e * nve;
+    double hq = 0.0;
+    for (int u = 0; u < 6; ++u) hq += Ae[6 * u + r] * He[tri6(u, q)];
+    Tb[x] = hq;
+  }
+  __syncthreads();
+  // pose-block terms per edge: (Ad_e^T H_e - N_e) Ad_e; N_e = Nm[:, 6e..6e+5]
+  for (int x = tid; x < k * 36; x += blockDim.x) {
+    const int e = x / 36, r = (x / 6) % 6, c = x % 6;
+    const double* Ae = Ad + 36 * e;
+    double t = 0.0;
+    for (int q = 0; q < 6; ++q) t += (Tb[36 * e + 6 * r + q] - Nm[r * mu + 6 * e + q]) * Ae[6 * q + c];
+    Tc[x] = t;
   }
   __syncthreads();
   const int th0 = 6 * k;  // theta offset in u-space
   for (int x = tid; x < m * m; x += blockDim.x) {
     const int r = x / m, c = x % m;
+    double v;
     if (r >= 6 && c >= 6) {
       const int ru = r - 6, cu = c - 6;
       double b = 0.0;
@@ -230,22 +254,12 @@ __global__ void __launch_bounds__(256) assemble_kernel(const AsmArgs A) {
       } else {
         b = fs[1 + tri4(ru - th0, cu - th0)];
       }
-      F[x] += b;
+      v = b - Ms[ru * mu + cu];
     } else if (r < 6 && c < 6) {
-      double s = 0.0;
-      for (int e = 0; e < k; ++e) {
-        const double* Ae = Ad + 36 * e;
-        const double* He = hs + e * nve;
-        // + Ad_e^T H_e Ad_e   - N_e Ad_e
-        for (int q = 0; q < 6; ++q) {
-          double hq = 0.0;
-          for (int u = 0; u < 6; ++u) hq += Ae[6 * u + r] * He[tri6(u, q)];
-          s += (hq - Nm[r * mu + 6 * e + q]) * Ae[6 * q + c];
-        }
-      }
-      F[x] = s;
+      v = 0.0;
+      for (int e = 0; e < k; ++e) v += Tc[36 * e + 6 * r + c];  // fixed edge order
     } else {
-      const int rr = r < 6 ? r : c;       // pose-i row (0..5)
+      const int rr = r < 6 ? r : c;          // pose-i row (0..5)
       const int cu = r < 6 ? c - 6 : r - 6;  // u-space column
       double b = 0.0;
       if (A.calib && cu >= th0) {
@@ -256,8 +270,9 @@ __global__ void __launch_bounds__(256) assemble_kernel(const AsmArgs A) {
         const int e = cu / 6, cc = cu % 6;
         for (int q = 0; q < 6; ++q) b -= Ad[36 * e + 6 * q + rr] * hs[e * nve + tri6(q, cc)];
       }
-      F[x] = Nm[rr * mu + cu] + b;
+      v = b + Nm[rr * mu + cu];  // B_iu - (T M T^T)_iu with T_i = -Ad^T
     }
+    F[x] = v;
   }
   for (int x = tid; x < m; x += blockDim.x) {
     double v;
@@ -347,8 +362,8 @@ struct FinalArgs {
   double* energy_out;
 };
 
-__global__ void __launch_bounds__(256) finalize_kernel(const FinalArgs A) {
-  if (trial_skipped(A.status)) return;
+
+__device__ __forceinline__ void finalize_energy(const FinalArgs& A) {
   __shared__ double sh[256];
   double s = 0.0;
   for (int x = threadIdx.x; x < A.n; x += 256) s += A.part_frame[(long long)x * kFrameVals];
@@ -359,6 +374,11 @@ __global__ void __launch_bounds__(256) finalize_kernel(const FinalArgs A) {
     __syncthreads();
   }
   if (threadIdx.x == 0) A.energy_out[0] = sh[0];
+}
+
+__global__ void __launch_bounds__(256) finalize_kernel(const FinalArgs A) {
+  if (trial_skipped(A.status)) return;
+  finalize_energy(A);
 }
 
 // ---------------------------------------------------------------- gauge (A5)
@@ -437,8 +457,7 @@ struct DecideArgs {
   Control* ctl;
 };
 
-__global__ void decide_kernel(const DecideArgs A) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+__device__ void gn_decide(const DecideArgs& A) {
   Control* c = A.ctl;
   int* st = A.status;
   c->accept = 0;
@@ -490,6 +509,16 @@ __global__ void decide_kernel(const DecideArgs A) {
   *A.cond = 0.0;
 }
 
+__global__ void decide_kernel(const DecideArgs A) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) gn_decide(A);
+}
+
+// single rank: the trial energy and the LM decision in one launch
+__global__ void __launch_bounds__(256) finalize_decide_kernel(const FinalArgs F, const DecideArgs D) {
+  if (!trial_skipped(F.status)) finalize_energy(F);  // uniform over the block
+  if (threadIdx.x == 0) gn_decide(D);
+}
+
 struct CopySpan {
   float* dst;
   const float* src;
@@ -501,13 +530,15 @@ struct AcceptArgs {
   int nspan;
 };
 
-__global__ void accept_kernel(const AcceptArgs A) {
-  if (!A.ctl->accept) return;
-  const long long stride = (long long)gridDim.x * blockDim.x;
-  for (int s = 0; s < A.nspan; ++s) {
-    const CopySpan sp = A.span[s];
-    for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < sp.n; x += stride) sp.dst[x] = sp.src[x];
-  }
+__global__ void __launch_bounds__(256) accept_kernel(const AcceptArgs A) {
+  if (!A.ctl->accept || blockIdx.y >= A.nspan) return;
+  const CopySpan sp = A.span[blockIdx.y];
+  const long long stride = (long long)gridDim.x * blockDim.x, t0 = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const bool vec = ((reinterpret_cast<uintptr_t>(sp.dst) | reinterpret_cast<uintptr_t>(sp.src)) & 15) == 0;
+  long long n4 = vec ? sp.n / 4 : 0;
+  for (long long x = t0; x < n4; x += stride)
+    reinterpret_cast<float4*>(sp.dst)[x] = reinterpret_cast<const float4*>(sp.src)[x];
+  for (long long x = 4 * n4 + t0; x < sp.n; x += stride) sp.dst[x] = sp.src[x];
 }
 
 }  // namespace dba
