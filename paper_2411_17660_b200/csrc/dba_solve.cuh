@@ -34,11 +34,15 @@
 
 namespace dba {
 
+#ifndef DBA_NOPRODUCER
+#define DBA_NOPRODUCER 0
+#endif
 constexpr int kSolveThreads = 256;
 constexpr int kCritWarp = 7;
 constexpr int kStageWarp = 3;       // shares the critical warp's scheduler; only issues cp.async
 constexpr int kTrailThreads = 192;  // warps 0,1,2,4,5,6
 constexpr int kMaxBand = 24;        // compiled limit on BW
+constexpr int kRing = 32;           // backward-sweep factor-row ring depth (hides the bulk-copy latency)
 
 struct SolveArgs {
   int nb, BW, calib;
@@ -64,13 +68,13 @@ __host__ __device__ inline long long solve_mid_len(int BW) {
 }
 
 struct SolveSmem {
-  size_t win, th, thL, z, thm, thLm, zm, dinv, pbuf, cbuf, tbuf, pairs, total;
+  size_t win, ring, th, thL, z, thm, thLm, zm, dinv, pbuf, cbuf, tbuf, pairs, bars, total;
 };
 __host__ __device__ inline SolveSmem solve_smem_layout(int nb, int BW, int calib) {
   SolveSmem s;
   size_t o = 0;
-  // the window is reused by the backward sweep as an 8-row cp.async ring
-  s.win = o; o += sizeof(double) * (size_t)((BW + 1) > 8 ? (BW + 1) : 8) * (BW + 1) * 36;
+  s.win = o; o += sizeof(double) * (size_t)(BW + 1) * (BW + 1) * 36;
+  s.ring = o; o += sizeof(double) * (size_t)kRing * BW * 36;  // backward sweep: L blocks of kRing rows
   s.th = o; o += sizeof(double) * (calib ? (size_t)nb * 24 + 16 : 0);
   s.thL = o; o += sizeof(double) * (calib ? (size_t)nb * 24 : 0);
   s.z = o; o += sizeof(double) * ((size_t)6 * nb + 4);
@@ -82,6 +86,8 @@ __host__ __device__ inline SolveSmem solve_smem_layout(int nb, int BW, int calib
   s.cbuf = o; o += sizeof(double) * 2 * 36;
   s.tbuf = o; o += sizeof(double) * 24;
   s.pairs = o; o += sizeof(short2) * (size_t)(BW * (BW + 1) / 2 + 1);
+  o = (o + 7) & ~size_t(7);
+  s.bars = o; o += sizeof(unsigned long long) * 2 * kRing;  // backward-sweep ring full/empty mbarriers
   s.total = (o + 15) & ~size_t(15);
   return s;
 }
@@ -182,6 +188,8 @@ struct ChainSm {
   double* cbuf;  // critical-warp scratch
   double* tbuf;  // theta panel
   short2* pairs;
+  double* ring;
+  unsigned long long* bars;
   int* fail;
 };
 
@@ -191,6 +199,9 @@ struct ChainSm {
 // diagonal block includes the critical warp's update).  ncols: offset of the theta
 // rows in th / z.  Writes factor rows [0, nrows) to Lband (off-diagonal L blocks) and
 // D_b^-1 to the diagonal slot of rows [0, npiv).
+#ifdef DBA_SOLVE_PROF
+__device__ long long g_prof[16];  // [role*2 + {work, barrier wait}] cycles, CTA 0
+#endif
 __device__ inline void chain_forward(const ChainSm& S, const double* band, double* Lband, int nrows, int npiv,
                                      int BW, int calib, int ncols, double lam) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -211,6 +222,9 @@ __device__ inline void chain_forward(const ChainSm& S, const double* band, doubl
   __syncthreads();
   int sb = 0;  // slot of block row b (= b % W1)
   for (int b = 0; b < npiv && !*S.fail; ++b) {
+#ifdef DBA_SOLVE_PROF
+    const long long pt0 = clock64();
+#endif
     const int amax = min(nrows - 1, b + BW);
     const int na = amax - b;
     const double* Db = S.dinv + 36 * (b & 1);  // D_b^-1
@@ -287,7 +301,17 @@ __device__ inline void chain_forward(const ChainSm& S, const double* band, doubl
           row_times(S.th + (size_t)b * 24 + 6 * tt, Db, S.tbuf + 6 * tt);
         }
       }
+#ifdef DBA_SOLVE_PROF
+      const long long pa = clock64();
+#endif
       asm volatile("bar.sync 1, %0;" ::"n"(kTrailThreads) : "memory");
+#ifdef DBA_SOLVE_PROF
+      const long long pb2 = clock64();
+      if (blockIdx.x == 0 && warp == 0 && lane == 0) {
+        g_prof[6] += pa - pt0;
+        g_prof[7] += pb2 - pa;
+      }
+#endif
       // trailing update S_ac -= L_ab S_cb^T (except (b+1,b+1)), border, rhs
       const int npair = na * (na + 1) / 2;
       const int n1 = npair * 3;
@@ -385,7 +409,19 @@ __device__ inline void chain_forward(const ChainSm& S, const double* band, doubl
       asm volatile("cp.async.commit_group;");
       asm volatile("cp.async.wait_all;" ::: "memory");
     }
+#ifdef DBA_SOLVE_PROF
+    __syncwarp();
+    const long long pt1 = clock64();
+#endif
     __syncthreads();
+#ifdef DBA_SOLVE_PROF
+    const long long pt2 = clock64();
+    if (blockIdx.x == 0 && lane == 0 && (crit || warp == 0 || warp == kStageWarp)) {
+      const int role = crit ? 0 : (warp == 0 ? 1 : 2);
+      g_prof[2 * role] += pt1 - pt0;
+      g_prof[2 * role + 1] += pt2 - pt1;
+    }
+#endif
     sb = (sb + 1 == W1) ? 0 : sb + 1;
   }
 }
@@ -431,7 +467,8 @@ __device__ inline bool theta_solve(const double* T, double* zt, double lam, doub
 // `ring` (>= 8 factor rows) streams Lband rows via cp.async; tmp (6 npiv) staging.
 template <int NS>
 __device__ inline void chain_backward(double* z, const double* thL, const double* xt, const double* Lband,
-                                      double* ring, int nrows, int npiv, int BW, int calib, double* tmp) {
+                                      double* ring, unsigned long long* bars, int nrows, int npiv, int BW, int calib,
+                                      double* tmp) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int W1 = BW + 1, NR = W1 * 36;
   for (int x = tid; x < 6 * npiv; x += kSolveThreads) {
@@ -448,43 +485,143 @@ __device__ inline void chain_backward(double* z, const double* thL, const double
   }
   __syncthreads();
   for (int x = tid; x < 6 * npiv; x += kSolveThreads) z[x] = tmp[x];
+  // sweep: rows a = nrows-1 .. 1 fold x_a into x_b, b in [a-BW, a-1].  The factor rows
+  // stream through a ring of RD slots: the staging warp refills a slot with one bulk
+  // async copy (TMA engine) once the sweep warp has released it (full/empty mbarrier
+  // pairs), so the sweep's critical path holds no copy issue and no proxy fence.
+  constexpr int RD = kRing;
+  const unsigned full0 = (unsigned)__cvta_generic_to_shared(bars), empty0 = full0 + 8 * RD;
+  const unsigned bytes = (unsigned)(BW * 36 * sizeof(double));
+  if (tid == 0)
+    for (int t = 0; t < RD; ++t) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(full0 + 8 * t));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(empty0 + 8 * t));
+    }
   __syncthreads();
-  if (warp == kCritWarp && nrows > 1) {
-    constexpr int RD = 8;
-    auto issue = [&](int a) {
-      if (a >= 1) {
-        const char* src = reinterpret_cast<const char*>(Lband + (size_t)a * NR);
-        const unsigned dst = (unsigned)__cvta_generic_to_shared(ring + (size_t)(a % RD) * NR);
-        for (int q = lane; q < NR / 2; q += 32)
-          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + 16 * q), "l"(src + 16 * q));
+  auto wait_bar = [](unsigned bar, unsigned parity) {
+    unsigned done = 0;
+    while (!done)
+      asm volatile(
+          "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+          "selp.u32 %0, 1, 0, p;\n\t}\n"
+          : "=r"(done)
+          : "r"(bar), "r"(parity)
+          : "memory");
+  };
+  if (warp == kStageWarp && lane == 0 && nrows > 1 && !DBA_NOPRODUCER) {
+    static_assert(RD == 32, "four batches of 8 slots");
+    unsigned fills = 0;  // 8 bits per batch of 8 slots: how often the batch was entered
+    for (int i = 0; nrows - 1 - i >= 1; ++i) {
+      const int a = nrows - 1 - i, slot = a % RD, batch = slot / 8;
+      const bool enter = i == 0 || slot % 8 == 7;
+      const unsigned use = (fills >> (8 * batch)) & 255u;
+      if (enter) fills += 1u << (8 * batch);
+      if (enter && use > 0) {  // wait for the sweep's use-th release of this batch
+        // the producer shares the sweep warp's scheduler: back off instead of spinning
+        for (unsigned done = 0;;) {
+          asm volatile(
+              "{\n\t.reg .pred p;\n\tmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+              "selp.u32 %0, 1, 0, p;\n\t}\n"
+              : "=r"(done)
+              : "r"(empty0 + 8 * batch), "r"((unsigned)(use - 1) & 1u)
+              : "memory");
+          if (done) break;
+          __nanosleep(64);
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the sweep's reads of the slot
       }
-      asm volatile("cp.async.commit_group;");
-    };
-    for (int t = 0; t < RD; ++t) issue(nrows - 1 - t);
-    for (int a = nrows - 1; a >= 1; --a) {
-      asm volatile("cp.async.wait_group %0;" ::"n"(RD - 1) : "memory");
-      __syncwarp();
-      const double* row = ring + (size_t)(a % RD) * NR;
-      double xr[6];
+      const unsigned dst = (unsigned)__cvta_generic_to_shared(ring + (size_t)slot * BW * 36);
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(full0 + 8 * slot), "r"(bytes)
+                   : "memory");
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                       dst),
+                   "l"(Lband + (size_t)a * NR), "r"(bytes), "r"(full0 + 8 * slot)
+                   : "memory");
+    }
+  } else if (warp == kCritWarp && nrows > 1) {
+#ifdef DBA_SOLVE_PROF
+    const long long qs0 = clock64();
+#endif
+    // register window with rotating row groups: slot (lane < 30, register j) belongs to
+    // group g = 5 j + lane / 6 (component lane % 6) and holds the partially folded z of
+    // row a-1-((g - gc) mod BW); group gc holds the row finalised in this step.  No data
+    // moves between lanes: the finished group reloads the row entering at distance BW.
+    const int gl = lane < 30 ? lane / 6 : 99, cl = lane % 6;
+    double zr[NS];
+    int gc = 0;
+    const int a0 = nrows - 1;
 #pragma unroll
-      for (int r = 0; r < 6; ++r) xr[r] = z[6 * a + r];
+    for (int j = 0; j < NS; ++j) {
+      const int g = 5 * j + gl, bp = a0 - 1 - g;
+      zr[j] = (g < BW && bp >= 0) ? z[6 * bp + cl] : 0.0;
+    }
+    double xr[6];
+#pragma unroll
+    for (int r = 0; r < 6; ++r) xr[r] = z[6 * a0 + r];
+    for (int i = 0; nrows - 1 - i >= 1; ++i) {
+      const int a = nrows - 1 - i, slot = a % RD;
+#ifndef DBA_NOWAIT
+      wait_bar(full0 + 8 * slot, (i / RD) & 1);
+#endif
+      const double* row = ring + (size_t)slot * BW * 36;
+      // branch-free so that all loads issue ahead of the FMA chains
+      double acc[NS];
+      bool fold[NS];
 #pragma unroll
       for (int j = 0; j < NS; ++j) {
-        const int q = lane + 32 * j;
-        const int bp = a - 1 - q / 6;
-        if (q < 6 * BW && bp >= 0 && bp < npiv) {
-          const double* blk = row + (BW - 1 - q / 6) * 36 + q % 6;
-          double acc = 0.0;
+        const int g = 5 * j + gl;
+        int d = g - gc;
+        d = d < 0 ? d + BW : d;
+        const int bp = a - 1 - d;  // this slot's row
+        fold[j] = g < BW && bp >= 0 && bp < npiv;
+        const double* blk = row + (fold[j] ? (BW - 1 - d) * 36 + cl : 0);
+        double v[6];
 #pragma unroll
-          for (int r = 0; r < 6; ++r) acc = fma(blk[6 * r], xr[r], acc);
-          z[6 * bp + q % 6] -= acc;
-        }
+        for (int r = 0; r < 6; ++r) v[r] = blk[6 * r];
+        acc[j] = 0.0;
+#pragma unroll
+        for (int r = 0; r < 6; ++r) acc[j] = fma(v[r], xr[r], acc[j]);
       }
+#pragma unroll
+      for (int j = 0; j < NS; ++j) zr[j] = fold[j] ? zr[j] - acc[j] : zr[j];
+      // x_{a-1} is final in group gc: broadcast it, store it, reload the group
+      const int jc = gc / 5, lc = 6 * (gc % 5);
+      double zc = zr[0];
+#pragma unroll
+      for (int j = 1; j < NS; ++j) zc = (jc == j) ? zr[j] : zc;
+#pragma unroll
+      for (int r = 0; r < 6; ++r) xr[r] = __shfl_sync(0xffffffffu, zc, lc + r);
       __syncwarp();
-      issue(a - RD);
+      // slots are released in batches of 8 (one arrive per batch keeps the
+      // barrier off the per-row critical path)
+      if (lane == 0 && !DBA_NOPRODUCER && slot % 8 == 0)
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(empty0 + 8 * (slot / 8)) : "memory");
+      if (lane < 30 && gl == gc % 5) z[6 * (a - 1) + cl] = zc;
+      {
+        const int bp = a - 1 - BW;
+        const double v = z[6 * (bp >= 0 ? bp : 0) + cl];
+        const bool take = gl == gc % 5;
+#pragma unroll
+        for (int j = 0; j < NS; ++j) zr[j] = (take && j == jc) ? (bp >= 0 ? v : 0.0) : zr[j];
+      }
+      gc = gc + 1 == BW ? 0 : gc + 1;
     }
-    asm volatile("cp.async.wait_all;" ::: "memory");
+#ifdef DBA_SOLVE_PROF
+    if (blockIdx.x == 0 && lane == 0 && nrows > 20) g_prof[14] += clock64() - qs0;
+#endif
   }
+#ifdef DBA_SOLVE_PROF
+  const long long qe0 = clock64();
+#endif
+  __syncthreads();
+#ifdef DBA_SOLVE_PROF
+  if (blockIdx.x == 0 && warp == kCritWarp && lane == 0 && nrows > 20) g_prof[15] += clock64() - qe0;
+#endif
+  if (tid == 0)
+    for (int t = 0; t < RD; ++t) {
+      asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(full0 + 8 * t));
+      asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(empty0 + 8 * t));
+    }
   __syncthreads();
 }
 
@@ -499,6 +636,8 @@ __device__ inline ChainSm chain_sm(unsigned char* smem, const SolveSmem& L, int*
   S.cbuf = reinterpret_cast<double*>(smem + L.cbuf);
   S.tbuf = reinterpret_cast<double*>(smem + L.tbuf);
   S.pairs = reinterpret_cast<short2*>(smem + L.pairs);
+  S.bars = reinterpret_cast<unsigned long long*>(smem + L.bars);
+  S.ring = reinterpret_cast<double*>(smem + L.ring);
   S.fail = fail;
   return S;
 }
@@ -531,7 +670,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const SolveArgs
     if (tid == 0) A.status[0] = 1;
     return;
   }
-  chain_backward<NS>(S.z, S.thL, S.z + 6 * nb, A.Lband, S.win, nb, nb, BW, A.calib, A.delta);
+  chain_backward<NS>(S.z, S.thL, S.z + 6 * nb, A.Lband, S.ring, S.bars, nb, nb, BW, A.calib, A.delta);
   for (int x = tid; x < 6 * nb + (A.calib ? 4 : 0); x += kSolveThreads) A.delta[x] = S.z[x];
 }
 
@@ -571,7 +710,13 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve2_kernel(const SolveArg
   }
   if (calib && tid < 4) S.z[6 * nb + tid] = A.y[6 * nb + tid];
   __syncthreads();
+#ifdef DBA_SOLVE_PROF
+  long long ph0 = clock64();
+#endif
   chain_forward(S, band, Lb, nrows, npiv, BW, calib, nb, lam);
+#ifdef DBA_SOLVE_PROF
+  long long ph1 = clock64();
+#endif
   // ---- export the middle rows (local rows npiv..nrows-1, columns >= npiv)
   const long long per = (long long)BW * BW * 36 + 6 * BW + (long long)BW * 24 + 16 + 4;
   double* ex = A.mid + cta * per;
@@ -639,7 +784,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve2_kernel(const SolveArg
     if (calib && tid == 0 && !fail)
       if (!theta_solve(M.th + (size_t)BW * 24, M.z + 6 * BW, lam, A.cond)) fail = 1;
     __syncthreads();
-    if (!fail) chain_backward<NS>(M.z, M.thL, M.z + 6 * BW, Lm, M.win, BW, BW, BWm, calib, A.delta);
+    if (!fail) chain_backward<NS>(M.z, M.thL, M.z + 6 * BW, Lm, M.ring, M.bars, BW, BW, BWm, calib, A.delta);
     for (int x = tid; x < 6 * BW + (calib ? 4 : 0); x += kSolveThreads) xsol[x] = M.z[x];
     __syncthreads();
     if (tid == 0 && fail) atomicExch(gfail, 1);
@@ -650,6 +795,9 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve2_kernel(const SolveArg
     if (tid == 0 && cta == 0) A.status[0] = 1;
     return;
   }
+#ifdef DBA_SOLVE_PROF
+  long long ph2 = clock64();
+#endif
   // ---- back-substitute this chain with the middle solution
   for (int x = tid; x < 6 * BW; x += kSolveThreads) {
     const int i = x / 6, s = x % 6;  // local middle row npiv + i
@@ -658,7 +806,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve2_kernel(const SolveArg
   if (tid < 4) xts[tid] = calib ? xsol[6 * BW + tid] : 0.0;
   __syncthreads();
   double* tmp = A.delta + (cta == 0 ? 0 : 6 * (m + BW));  // staging inside this chain's output range
-  chain_backward<NS>(S.z, S.thL, xts, Lb, S.win, nrows, npiv, BW, calib, tmp);
+  chain_backward<NS>(S.z, S.thL, xts, Lb, S.ring, S.bars, nrows, npiv, BW, calib, tmp);
   for (int x = tid; x < 6 * npiv; x += kSolveThreads) {
     const int a = x / 6, s = x % 6;
     A.delta[6 * (cta == 0 ? a : nb - 1 - a) + s] = S.z[x];
@@ -667,6 +815,14 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve2_kernel(const SolveArg
     for (int x = tid; x < 6 * BW; x += kSolveThreads) A.delta[6 * m + x] = xsol[x];
     if (calib && tid < 4) A.delta[6 * nb + tid] = xsol[6 * BW + tid];
   }
+#ifdef DBA_SOLVE_PROF
+  if (cta == 0 && tid == 0) {
+    const long long ph3 = clock64();
+    g_prof[10] += ph1 - ph0;  // forward
+    g_prof[11] += ph2 - ph1;  // export + middle + grid syncs
+    g_prof[12] += ph3 - ph2;  // backward + writes
+  }
+#endif
 }
 
 }  // namespace dba
