@@ -14,6 +14,7 @@
 #include <climits>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <set>
@@ -106,6 +107,11 @@ struct dba_plan {
     std::vector<std::pair<int, int>> pass_ev, solve_ev;
     long long launches = 0, pass_launches = 0, solve_launches = 0;
     double pass_ms = 0.0, solve_ms = 0.0;
+    // DBA_TIMELINE=1 (diagnostic): an event after every launch; per-label time from the
+    // previous event (kernel + launch gap), printed at each resolve
+    bool timeline = false;
+    std::vector<std::pair<const char*, cudaEvent_t>> marks;
+    std::vector<std::pair<const char*, double>> tl_sum;
   } prof;
 };
 
@@ -650,9 +656,38 @@ int ev_pair(Ctx& c, std::pair<int, int>& out) {
   return DBA_OK;
 }
 
+void mark(Ctx& c, const char* label) {
+  auto& pr = c.p->prof;
+  if (!pr.timeline) return;
+  cudaEvent_t e;
+  if (cudaEventCreate(&e) != cudaSuccess) return;
+  cudaEventRecord(e, c.st);
+  pr.marks.emplace_back(label, e);
+}
+
 // accumulate the recorded event pairs (call after a stream synchronisation)
 void prof_resolve(dba_plan* p) {
   auto& pr = p->prof;
+  if (pr.timeline && pr.marks.size() > 1) {
+    for (size_t i = 1; i < pr.marks.size(); ++i) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, pr.marks[i - 1].second, pr.marks[i].second);
+      bool found = false;
+      for (auto& t : pr.tl_sum)
+        if (!std::strcmp(t.first, pr.marks[i].first)) {
+          t.second += ms;
+          found = true;
+        }
+      if (!found) pr.tl_sum.emplace_back(pr.marks[i].first, (double)ms);
+    }
+    for (auto& m : pr.marks) cudaEventDestroy(m.second);
+    pr.marks.clear();
+    for (auto& t : pr.tl_sum) std::fprintf(stderr, "[dba timeline] %-10s %9.3f ms\n", t.first, t.second);
+    pr.tl_sum.clear();
+  } else {
+    for (auto& m : pr.marks) cudaEventDestroy(m.second);
+    pr.marks.clear();
+  }
   for (auto& e : pr.pass_ev) {
     float ms = 0.f;
     if (cudaEventElapsedTime(&ms, pr.pool[e.first], pr.pool[e.second]) == cudaSuccess) pr.pass_ms += ms;
@@ -717,9 +752,18 @@ int launch_prep(Ctx& c, int cur, int nxt, bool init) {
   a.lin = c.at<EdgeLin>(p->L.lin);
   a.back = c.at<EdgeBack>(p->L.back);
   a.adj = c.at<double>(p->L.adj);
-  const int n = p->N + p->EL + 1;
-  prep_kernel<<<(n + 31) / 32, 32, 0, c.st>>>(a);  // one warp per block: spread the fp64 work over SMs
+  // phase 0: one thread per pose (exp-map retraction) + intrinsics; phase 1: one per
+  // edge slot (relative poses, adjoints) reading phase 0's poses; one warp per block
+  // spreads the fp64 work over the SMs
+  a.phase = 0;
+  prep_kernel<<<(p->N + 1 + 31) / 32, 32, 0, c.st>>>(a);
   p->prof.launches++;
+  if (p->EL > 0) {
+    a.phase = 1;
+    prep_kernel<<<(p->EL + 31) / 32, 32, 0, c.st>>>(a);
+    p->prof.launches++;
+  }
+  mark(c, "prep");
   return cuda_status(cudaGetLastError());
 }
 
@@ -734,6 +778,7 @@ int launch_pass_t(Ctx& c, const PassArgs& a) {
     DBA_CUDA(cudaEventRecord(pr.pool[ev.first], c.st));
   }
   k<<<c.p->G, kPassThreads, c.p->pass_smem, c.st>>>(a);
+  mark(c, "pass");
   pr.launches++;
   pr.pass_launches++;
   if (pr.on) {
@@ -837,7 +882,8 @@ int launch_system(Ctx& c, int slot, bool decide = false) {
     a.gstate = c.at<double>(p->L.gstate[slot]);
     const size_t smem = assemble_smem_bytes(std::max(p->kmax, 1), p->calib);
     DBA_CUDA(cudaFuncSetAttribute(assemble_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    assemble_kernel<<<p->NL, 256, smem, c.st>>>(a);
+    assemble_kernel<<<p->NL, 512, smem, c.st>>>(a);
+  mark(c, "assemble");
     p->prof.launches++;
     DBA_CUDA(cudaGetLastError());
   }
@@ -851,6 +897,7 @@ int launch_system(Ctx& c, int slot, bool decide = false) {
     g.sys = c.at<double>(p->L.sys[slot]);
     const int threads = 256, warps = threads / 32;
     gather_kernel<<<(p->n_units + warps - 1) / warps, threads, 0, c.st>>>(g);
+  mark(c, "gather");
     p->prof.launches++;
     DBA_CUDA(cudaGetLastError());
   }
@@ -862,10 +909,12 @@ int launch_system(Ctx& c, int slot, bool decide = false) {
   const bool multi = c.comm && p->nranks > 1;
   if (decide && !multi) {
     finalize_decide_kernel<<<1, 256, 0, c.st>>>(f, decide_args(c));
+  mark(c, "fin+decide");
     p->prof.launches++;
     return cuda_status(cudaGetLastError());
   }
   finalize_kernel<<<1, 256, 0, c.st>>>(f);
+  mark(c, "finalize");
   p->prof.launches++;
   DBA_CUDA(cudaGetLastError());
   if (multi) {
@@ -919,6 +968,7 @@ int launch_solve(Ctx& c, int slot) {
   } else {
     kern<<<1, kSolveThreads, p->solve_smem, c.st>>>(a);
   }
+  mark(c, "solve");
   pr.launches++;
   pr.solve_launches++;
   if (pr.on) {
@@ -950,7 +1000,8 @@ int launch_accept(Ctx& c) {
        (long long)p->NL * p->P);
   span(p->L.sys[0], p->L.sys[1], 2 * p->sys_len);
   span(p->L.gstate[0], p->L.gstate[1], 2LL * (6 * kMaxOutDegree + 8));
-  accept_kernel<<<dim3(std::max(p->G / 2, 1), a.nspan), 256, 0, c.st>>>(a);
+  accept_kernel<<<dim3(2 * std::max(p->G, 1), a.nspan), 256, 0, c.st>>>(a);
+  mark(c, "accept");
   p->prof.launches++;
   return cuda_status(cudaGetLastError());
 }
@@ -1124,6 +1175,7 @@ int dba_solve(dba_plan* p, const dba_options* o, const dba_buffers* b, dba_repor
 }
 
 int dba_plan_set_profiling(dba_plan* p, int32_t enable) {
+  if (p) p->prof.timeline = enable && std::getenv("DBA_TIMELINE") != nullptr;
   if (!p) return DBA_EINVAL;
   p->prof.on = enable != 0;
   return DBA_OK;

@@ -20,6 +20,7 @@ namespace dba {
 
 struct PrepArgs {
   int N, EL, init, calib, theta_off;
+  int phase;  // 0: per-pose retraction (+ intrinsics), 1: per-edge constants from both states
   double tmax;
   const int* status;
   const int* ridx;
@@ -61,7 +62,15 @@ __device__ inline Pose64 stepped_pose(const PrepArgs& A, int k, const double xi[
 
 __global__ void prep_kernel(const PrepArgs A) {
   if (trial_skipped(A.status)) return;
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x + (A.phase == 1 ? A.N : 0);
+  if (A.phase == 0 && t == A.N) {  // intrinsics
+    for (int c = 0; c < 4; ++c) {
+      const double d = (A.calib && !A.init) ? A.delta[A.theta_off + c] : 0.0;
+      A.intr_n[c] = A.intr_c[c] + d;
+    }
+    return;
+  }
+  if (A.phase == 0 ? t > A.N : t >= A.N + A.EL) return;
   if (t < A.N) {
     double xi[6];
     clamped_xi(A, t, xi);
@@ -75,11 +84,13 @@ __global__ void prep_kernel(const PrepArgs A) {
     const int s = t - A.N;
     const int i = A.slot_i[s], j = A.slot_j[s];
     double xi_i[6], xi_j[6];
-    clamped_xi(A, i, xi_i);
-    clamped_xi(A, j, xi_j);
+    for (int c = 0; c < 6; ++c) {  // clamped steps and stepped poses from phase 0
+      xi_i[c] = A.xi_out[6 * i + c];
+      xi_j[c] = A.xi_out[6 * j + c];
+    }
     const Pose64 ci = load_pose(A.poses_c + 7 * i), cj = load_pose(A.poses_c + 7 * j);
     const Pose64 gc = compose(cj, inverse(ci));
-    const Pose64 gn = compose(stepped_pose(A, j, xi_j), inverse(stepped_pose(A, i, xi_i)));
+    const Pose64 gn = compose(load_pose(A.poses_n + 7 * j), inverse(load_pose(A.poses_n + 7 * i)));
     double Rn[9], Rc[9], Ac[36], An[36];
     quat_to_rot(gn.q, Rn);
     quat_to_rot(gc.q, Rc);
@@ -104,11 +115,6 @@ __global__ void prep_kernel(const PrepArgs A) {
     A.lin[s] = el;
     A.back[s] = eb;
     for (int c = 0; c < 36; ++c) A.adj[36 * (size_t)s + c] = An[c];
-  } else if (t == A.N + A.EL) {
-    for (int c = 0; c < 4; ++c) {
-      const double d = (A.calib && !A.init) ? A.delta[A.theta_off + c] : 0.0;
-      A.intr_n[c] = A.intr_c[c] + d;
-    }
   }
 }
 
@@ -160,7 +166,7 @@ __host__ __device__ inline size_t assemble_smem_bytes(int kmax, bool calib) {
   return sizeof(double) * mu * mu;
 }
 
-__global__ void __launch_bounds__(256) assemble_kernel(const AsmArgs A) {
+__global__ void __launch_bounds__(512) assemble_kernel(const AsmArgs A) {
   if (trial_skipped(A.status)) return;
   extern __shared__ double Ms[];  // M = sum_p v_p v_p^T / C_p over u-space (mu x mu)
   __shared__ double Ad[kMaxOutDegree * 36];
@@ -345,6 +351,7 @@ __global__ void gather_kernel(const GatherArgs A) {
   for (int e = lane; e < n; e += 32) {
     const int r = e / u.cols, c = e % u.cols;
     double s = 0.0;
+#pragma unroll 4
     for (int q = u.c0; q < u.c1; ++q) {
       const Contrib cb = A.contrib[q];
       s += u.trans ? A.Fbuf[cb.src + (long long)c * cb.stride + r] : A.Fbuf[cb.src + (long long)r * cb.stride + c];
@@ -536,6 +543,7 @@ __global__ void __launch_bounds__(256) accept_kernel(const AcceptArgs A) {
   const long long stride = (long long)gridDim.x * blockDim.x, t0 = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   const bool vec = ((reinterpret_cast<uintptr_t>(sp.dst) | reinterpret_cast<uintptr_t>(sp.src)) & 15) == 0;
   long long n4 = vec ? sp.n / 4 : 0;
+#pragma unroll 4
   for (long long x = t0; x < n4; x += stride)
     reinterpret_cast<float4*>(sp.dst)[x] = reinterpret_cast<const float4*>(sp.src)[x];
   for (long long x = 4 * n4 + t0; x < sp.n; x += stride) sp.dst[x] = sp.src[x];
