@@ -174,6 +174,33 @@ class ClockSampler:
                 "source": "nvml" if self.nvml is not None else "nvidia-smi"}
 
 
+def compute_roofline(inp, H, W, pass_ms):
+    """FP32-pipe view of the same pass: SURVEY §8d algorithmic FLOPs (230 per edge-pixel
+    for residual/Jacobians/H_jj/E/C, 2 per entry of the per-frame Schur GEMM M_ext = V V^T
+    with 6k+2 rows) against the nominal FMA peak (SMs x 128 lanes x 2 x SM clock)."""
+    import numpy as np
+    import torch
+    P = H * W
+    k = np.bincount(np.asarray(inp["ii"])[np.asarray(inp["local"])], minlength=1)
+    k = k[k > 0]
+    m = 6 * k + 2
+    flops = 230.0 * len(inp["local"]) * P + float(np.sum(m * (m + 1))) * P
+    props = torch.cuda.get_device_properties(0)
+    clk_ghz = 1.965
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        clk_ghz = pynvml.nvmlDeviceGetMaxClockInfo(pynvml.nvmlDeviceGetHandleByIndex(0),
+                                                   pynvml.NVML_CLOCK_SM) / 1000.0
+    except Exception:
+        pass
+    peak = props.multi_processor_count * 128 * 2 * clk_ghz * 1e-3  # TFLOP/s
+    achieved = flops / (pass_ms * 1e-3) * 1e-12
+    return {"bound": "fp32", "flop_per_launch": flops, "achieved": achieved, "peak": peak,
+            "unit": "TFLOP/s", "frac": achieved / peak,
+            "peak_kind": "nominal fp32 FMA (measured FFMA microbenchmark: 122-127 FFMA/clk/SM)"}
+
+
 def build_inputs(keyframes, rank, nranks):
     """Scene, graph and THIS rank's flow rows (local edges in input order)."""
     import numpy as np
@@ -312,7 +339,7 @@ def main():
     solver.set_profiling(True)
     st = torch.cuda.current_stream()
     total_ms = 0.0
-    trials = []
+    trials, accepted = [], []
     with ClockSampler(local_rank) as clk:
         for _ in range(args.steps):
             flush.zero_()
@@ -327,6 +354,7 @@ def main():
             barrier()
             total_ms += e0.elapsed_time(e1)
             trials.append(rep.trials)
+            accepted.append(rep.iterations_run)
     solver.set_profiling(False)
     stats = solver.stats(reset=True)
     t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
@@ -399,6 +427,11 @@ def main():
             "config": config_dict(args, world),
             "gn_iters_per_sec": n_trials / (total_ms * 1e-3),
             "gn_trials_per_step": n_trials / args.steps,
+            "gn_accepted_per_step": sum(accepted) / args.steps,
+            "note_trials": ("a GN trial = linearise + reduced solve + back-substitution + "
+                            "relinearise; trials rejected by the LM test (energy increase, here "
+                            "at the fp32 noise floor after ~4 iterations) are counted: each does "
+                            "the full work"),
             "ms_per_gn_iter": total_ms / max(n_trials, 1),
             "final_energy": rep.final_energy, "initial_energy": rep.initial_energy,
             "roofline": {"kernel": "dba::pass_kernel (fused back-substitute + linearise + Schur)",
@@ -407,7 +440,8 @@ def main():
                          "bytes_per_launch": bytes_per_pass, "ms_per_launch": pass_ms,
                          "solve_ms_per_launch": stats["solve_ms"] / max(stats["solve_launches"], 1),
                          "pass_share_of_step": stats["pass_ms"] / max(total_ms, 1e-9),
-                         "solve_share_of_step": stats["solve_ms"] / max(total_ms, 1e-9)},
+                         "solve_share_of_step": stats["solve_ms"] / max(total_ms, 1e-9),
+                         "compute": compute_roofline(inp, H, W, pass_ms)},
             "gpu_launches": int(stats["launches"]),
             "e2e": e2e,
             "cpu_baseline": cpu,
