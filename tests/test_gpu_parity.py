@@ -207,3 +207,25 @@ def test_two_sided_solve_parity(torch_cuda, calib, keyframes, radius):
     te, ae = pose_errors(Po.cpu().numpy(), ref.poses)
     assert te < REL_TOL, te
     assert abs(rep.final_energy - rrep.final_energy) <= REL_TOL * rrep.initial_energy
+
+
+@pytest.mark.parametrize("nranks", [2, 3])
+def test_sharded_partial_systems_sum_to_full(torch_cuda, nranks):
+    """Edge sharding by source frame: each rank's partial reduced system
+    (what the NCCL all-reduce sums) adds up to the single-rank system.  Ranks run one
+    after another on this GPU, each without a communicator (no cross-rank waits)."""
+    from paper_2411_17660_b200 import dba
+    wl = small_workload("C2", keyframes=12, radius=3)
+    N, H, W = len(wl.frames), wl.flow.shape[1], wl.flow.shape[2]
+    full = dba.DBASolver(wl.ii, wl.jj, N, H, W, wl.fixed)
+    S, y, e = full.build_system(wl.poses0, wl.disps0, wl.intr0, wl.flow)
+    Ss, ys, es = np.zeros_like(S), np.zeros_like(y), 0.0
+    for r in range(nranks):
+        part = dba.DBASolver(wl.ii, wl.jj, N, H, W, wl.fixed, rank=r, nranks=nranks)
+        Sr, yr, er = part.build_system(wl.poses0, wl.disps0, wl.intr0, wl.flow[part.local_edges])
+        Ss += Sr
+        ys += yr
+        es += er
+    assert _rel(Ss, S) < 1e-10, _rel(Ss, S)
+    assert _rel(ys, y) < 1e-10, _rel(ys, y)
+    assert abs(es - e) <= 1e-10 * e
