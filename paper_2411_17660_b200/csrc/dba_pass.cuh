@@ -140,6 +140,21 @@ __host__ __device__ inline PassSmem pass_smem_layout(int kmax, bool calib, bool 
   return s;
 }
 
+// packed fp32x2 FMA (sm_100): lanes (lo, hi) each fmaf-rounded
+__device__ __forceinline__ unsigned long long ffma2(unsigned long long a, unsigned long long b,
+                                                    unsigned long long c) {
+  unsigned long long d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ unsigned long long splat2(float a) {
+  const unsigned long long u = __float_as_uint(a);
+  return u | (u << 32);
+}
+__device__ __forceinline__ unsigned long long pack2(float2 v) {
+  return (unsigned long long)__float_as_uint(v.x) | ((unsigned long long)__float_as_uint(v.y) << 32);
+}
+
 // per edge-pixel geometry at one state
 struct PixTerms {
   bool ok;
@@ -248,9 +263,12 @@ __global__ void __launch_bounds__(kPassThreads, 1) pass_kernel(const PassArgs A)
       gk0 = (kSub * g) / G;
       gk1 = (kSub * (g + 1)) / G;
     }
-    float Macc[32];
+    // GEMM accumulators as float pairs: Macc2[4 r + q] = (M[r][2q], M[r][2q+1]) of the
+    // thread's 4x8 tile, updated with packed FFMA2 (two fp32 FMAs per instruction,
+    // each rounded exactly like FFMA)
+    unsigned long long Macc2[16];
 #pragma unroll
-    for (int x = 0; x < 32; ++x) Macc[x] = 0.f;
+    for (int x = 0; x < 16; ++x) Macc2[x] = 0ull;
     float hacc[kEdgeSlots][28];  // per-edge H_jj, g_j, energy of this warp's units (whole segment)
 #pragma unroll
     for (int s = 0; s < kEdgeSlots; ++s)
@@ -426,17 +444,31 @@ __global__ void __launch_bounds__(kPassThreads, 1) pass_kernel(const PassArgs A)
 #pragma unroll
           for (int s = 0; s < kEdgeSlots; ++s) {
             if (s != slot) continue;
+            // J_u[1] = 0 and J_v[0] = 0: the structurally zero terms are skipped
+            // (H_01 has none), which leaves every other sum unchanged bit for bit
             int o = 0;
 #pragma unroll
             for (int r = 0; r < 6; ++r)
 #pragma unroll
               for (int c = r; c < 6; ++c) {
-                hacc[s][o] = fmaf(T.wu * Ju[r], Ju[c], fmaf(T.wv * Jv[r], Jv[c], hacc[s][o]));
+                const bool zu = r == 1 || c == 1, zv = r == 0 || c == 0;
+                if (!zu && !zv)
+                  hacc[s][o] = fmaf(T.wu * Ju[r], Ju[c], fmaf(T.wv * Jv[r], Jv[c], hacc[s][o]));
+                else if (!zu)
+                  hacc[s][o] = fmaf(T.wu * Ju[r], Ju[c], hacc[s][o]);
+                else if (!zv)
+                  hacc[s][o] = fmaf(T.wv * Jv[r], Jv[c], hacc[s][o]);
                 ++o;
               }
 #pragma unroll
-            for (int r = 0; r < 6; ++r)
-              hacc[s][21 + r] = fmaf(T.wu * T.ru, Ju[r], fmaf(T.wv * T.rv, Jv[r], hacc[s][21 + r]));
+            for (int r = 0; r < 6; ++r) {
+              if (r == 0)
+                hacc[s][21 + r] = fmaf(T.wu * T.ru, Ju[r], hacc[s][21 + r]);
+              else if (r == 1)
+                hacc[s][21 + r] = fmaf(T.wv * T.rv, Jv[r], hacc[s][21 + r]);
+              else
+                hacc[s][21 + r] = fmaf(T.wu * T.ru, Ju[r], fmaf(T.wv * T.rv, Jv[r], hacc[s][21 + r]));
+            }
             hacc[s][27] += en;
           }
           if (CALIB) {
@@ -547,11 +579,11 @@ __global__ void __launch_bounds__(kPassThreads, 1) pass_kernel(const PassArgs A)
           const float2 b0 = row[(cb >> 1)], b1 = row[(cb >> 1) + 1], b2 = row[(cb >> 1) + 2],
                        b3 = row[(cb >> 1) + 3];
           const float av[4] = {a0.x, a0.y, a1.x, a1.y};
-          const float bv[8] = {b0.x, b0.y, b1.x, b1.y, b2.x, b2.y, b3.x, b3.y};
+          const unsigned long long bp[4] = {pack2(b0), pack2(b1), pack2(b2), pack2(b3)};
 #pragma unroll
           for (int r = 0; r < 4; ++r)
 #pragma unroll
-            for (int c = 0; c < 8; ++c) Macc[8 * r + c] = fmaf(av[r], bv[c], Macc[8 * r + c]);
+            for (int q = 0; q < 4; ++q) Macc2[4 * r + q] = ffma2(splat2(av[r]), bp[q], Macc2[4 * r + q]);
         }
       }
       __syncthreads();
@@ -573,7 +605,10 @@ __global__ void __launch_bounds__(kPassThreads, 1) pass_kernel(const PassArgs A)
       // GEMM partials of every (tile, pixel group) thread -> Mg[x][tid] (aliases U)
       if (tI >= 0) {
 #pragma unroll
-        for (int x = 0; x < 32; ++x) Mg[x * kPassThreads + tid] = Macc[x];
+        for (int x = 0; x < 32; ++x) {
+          const unsigned long long v = Macc2[x >> 1];
+          Mg[x * kPassThreads + tid] = __uint_as_float((unsigned)((x & 1) ? (v >> 32) : v));
+        }
       }
     }
     // per-frame values: fixed-order block reduction (float64 across warps)
