@@ -644,6 +644,31 @@ struct Ctx {
   }
 };
 
+// every library kernel is launched with programmatic stream serialisation (PDL): the
+// next kernel is scheduled while its predecessor runs and waits in pdl_enter()
+template <typename... KArgs, typename... Args>
+int launch(Ctx& c, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, bool coop, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = c.st;
+  cudaLaunchAttribute at[2];
+  int n = 0;
+  at[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[n].val.programmaticStreamSerializationAllowed = 1;
+  ++n;
+  if (coop) {
+    at[n].id = cudaLaunchAttributeCooperative;
+    at[n].val.cooperative = 1;
+    ++n;
+  }
+  cfg.attrs = at;
+  cfg.numAttrs = n;
+  c.p->prof.launches++;
+  return cuda_status(cudaLaunchKernelEx(&cfg, kern, args...));
+}
+
 int ev_pair(Ctx& c, std::pair<int, int>& out) {
   auto& pr = c.p->prof;
   while ((int)pr.pool.size() < pr.used + 2) {
@@ -756,15 +781,13 @@ int launch_prep(Ctx& c, int cur, int nxt, bool init) {
   // edge slot (relative poses, adjoints) reading phase 0's poses; one warp per block
   // spreads the fp64 work over the SMs
   a.phase = 0;
-  prep_kernel<<<(p->N + 1 + 31) / 32, 32, 0, c.st>>>(a);
-  p->prof.launches++;
+  if (int s = launch(c, prep_kernel, dim3((p->N + 1 + 31) / 32), dim3(32), 0, false, a)) return s;
   if (p->EL > 0) {
     a.phase = 1;
-    prep_kernel<<<(p->EL + 31) / 32, 32, 0, c.st>>>(a);
-    p->prof.launches++;
+    if (int s = launch(c, prep_kernel, dim3((p->EL + 31) / 32), dim3(32), 0, false, a)) return s;
   }
   mark(c, "prep");
-  return cuda_status(cudaGetLastError());
+  return DBA_OK;
 }
 
 template <bool CALIB>
@@ -777,9 +800,8 @@ int launch_pass_t(Ctx& c, const PassArgs& a) {
     if (int s = ev_pair(c, ev)) return s;
     DBA_CUDA(cudaEventRecord(pr.pool[ev.first], c.st));
   }
-  k<<<c.p->G, kPassThreads, c.p->pass_smem, c.st>>>(a);
+  if (int s = launch(c, k, dim3(c.p->G), dim3(kPassThreads), c.p->pass_smem, false, a)) return s;
   mark(c, "pass");
-  pr.launches++;
   pr.pass_launches++;
   if (pr.on) {
     DBA_CUDA(cudaEventRecord(pr.pool[ev.second], c.st));
@@ -882,10 +904,8 @@ int launch_system(Ctx& c, int slot, bool decide = false) {
     a.gstate = c.at<double>(p->L.gstate[slot]);
     const size_t smem = assemble_smem_bytes(std::max(p->kmax, 1), p->calib);
     DBA_CUDA(cudaFuncSetAttribute(assemble_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    assemble_kernel<<<p->NL, 512, smem, c.st>>>(a);
+    if (int s = launch(c, assemble_kernel, dim3(p->NL), dim3(512), smem, false, a)) return s;
   mark(c, "assemble");
-    p->prof.launches++;
-    DBA_CUDA(cudaGetLastError());
   }
   if (p->n_units > 0) {
     GatherArgs g;
@@ -896,10 +916,8 @@ int launch_system(Ctx& c, int slot, bool decide = false) {
     g.Fbuf = c.at<double>(p->L.Fbuf);
     g.sys = c.at<double>(p->L.sys[slot]);
     const int threads = 256, warps = threads / 32;
-    gather_kernel<<<(p->n_units + warps - 1) / warps, threads, 0, c.st>>>(g);
+    if (int s = launch(c, gather_kernel, dim3((p->n_units + warps - 1) / warps), dim3(threads), 0, false, g)) return s;
   mark(c, "gather");
-    p->prof.launches++;
-    DBA_CUDA(cudaGetLastError());
   }
   FinalArgs f;
   f.n = p->nseg;
@@ -908,15 +926,12 @@ int launch_system(Ctx& c, int slot, bool decide = false) {
   f.energy_out = c.at<double>(p->L.sys[slot]) + p->energy_off;
   const bool multi = c.comm && p->nranks > 1;
   if (decide && !multi) {
-    finalize_decide_kernel<<<1, 256, 0, c.st>>>(f, decide_args(c));
+    if (int s = launch(c, finalize_decide_kernel, dim3(1), dim3(256), 0, false, f, decide_args(c))) return s;
   mark(c, "fin+decide");
-    p->prof.launches++;
-    return cuda_status(cudaGetLastError());
+    return DBA_OK;
   }
-  finalize_kernel<<<1, 256, 0, c.st>>>(f);
+  if (int s = launch(c, finalize_kernel, dim3(1), dim3(256), 0, false, f)) return s;
   mark(c, "finalize");
-  p->prof.launches++;
-  DBA_CUDA(cudaGetLastError());
   if (multi) {
     if (!nccl().ok) return DBA_ENCCL;
     double* s = c.at<double>(p->L.sys[slot]);
@@ -962,14 +977,9 @@ int launch_solve(Ctx& c, int slot) {
     if (int s2 = ev_pair(c, ev)) return s2;
     DBA_CUDA(cudaEventRecord(pr.pool[ev.first], c.st));
   }
-  if (p->two_sided) {
-    void* args[] = {&a};
-    DBA_CUDA(cudaLaunchCooperativeKernel((const void*)kern, dim3(2), dim3(kSolveThreads), args, p->solve_smem, c.st));
-  } else {
-    kern<<<1, kSolveThreads, p->solve_smem, c.st>>>(a);
-  }
+  if (int s = launch(c, kern, dim3(p->two_sided ? 2 : 1), dim3(kSolveThreads), p->solve_smem, p->two_sided != 0, a))
+    return s;
   mark(c, "solve");
-  pr.launches++;
   pr.solve_launches++;
   if (pr.on) {
     DBA_CUDA(cudaEventRecord(pr.pool[ev.second], c.st));
@@ -980,9 +990,8 @@ int launch_solve(Ctx& c, int slot) {
 
 int launch_decide(Ctx& c) {
   dba_plan* p = c.p;
-  decide_kernel<<<1, 32, 0, c.st>>>(decide_args(c));
-  p->prof.launches++;
-  return cuda_status(cudaGetLastError());
+  (void)p;
+  return launch(c, decide_kernel, dim3(1), dim3(32), 0, false, decide_args(c));
 }
 
 // accepted trial (slot 1) -> current iterate (slot 0)
@@ -1000,10 +1009,9 @@ int launch_accept(Ctx& c) {
        (long long)p->NL * p->P);
   span(p->L.sys[0], p->L.sys[1], 2 * p->sys_len);
   span(p->L.gstate[0], p->L.gstate[1], 2LL * (6 * kMaxOutDegree + 8));
-  accept_kernel<<<dim3(2 * std::max(p->G, 1), a.nspan), 256, 0, c.st>>>(a);
+  if (int s = launch(c, accept_kernel, dim3(2 * std::max(p->G, 1), a.nspan), dim3(256), 0, false, a)) return s;
   mark(c, "accept");
-  p->prof.launches++;
-  return cuda_status(cudaGetLastError());
+  return DBA_OK;
 }
 
 int upload_control(Ctx& c, double lam, double Ec) {
@@ -1063,9 +1071,7 @@ int gauge_sum(Ctx& c, const float* d, double* out) {
   dba_plan* p = c.p;
   const int g = p->gauge_frame;
   const int frame = (g >= p->f0 && g < p->f1) ? g : -1;
-  logsum_kernel<<<1, 256, 0, c.st>>>(d, frame, p->P, out);
-  p->prof.launches++;
-  DBA_CUDA(cudaGetLastError());
+  if (int s = launch(c, logsum_kernel, dim3(1), dim3(256), 0, false, d, frame, p->P, out)) return s;
   if (c.comm && p->nranks > 1 && nccl().ok)
     if (nccl().AllReduce(out, out, 1, ncclDouble, ncclSum, c.comm, c.st) != ncclSuccess) return DBA_ENCCL;
   return DBA_OK;
@@ -1163,9 +1169,8 @@ int dba_solve(dba_plan* p, const dba_options* o, const dba_buffers* b, dba_repor
     g.d = b->disps_out;
     g.poses = b->poses_out;
     const long long n = std::max<long long>((long long)p->NL * p->P, p->N);
-    gauge_apply_kernel<<<(unsigned)((n + 255) / 256), 256, 0, c.st>>>(g);
-    p->prof.launches++;
-    DBA_CUDA(cudaGetLastError());
+    if ((s = launch(c, gauge_apply_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, false, g)))
+      return rep->status = s;
     DBA_CUDA(cudaMemcpyAsync(&rep->scale, gsum + 2, sizeof(double), cudaMemcpyDeviceToHost, c.st));
   }
   DBA_CUDA(cudaStreamSynchronize(c.st));

@@ -184,6 +184,7 @@ __device__ __forceinline__ PixTerms pix_terms(const float R[9], const float t[3]
 
 template <bool CALIB>
 __global__ void __launch_bounds__(kPassThreads, 1) pass_kernel(const PassArgs A) {
+  pdl_enter();
   if (trial_skipped(A.status)) return;
   extern __shared__ __align__(16) unsigned char smem[];
   constexpr int NVE = kEdgeVals + (CALIB ? kCalibVals : 0);

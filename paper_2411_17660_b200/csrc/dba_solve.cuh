@@ -645,6 +645,7 @@ __device__ inline ChainSm chain_sm(unsigned char* smem, const SolveSmem& L, int*
 // one-sided solve (small systems)
 template <int NS>
 __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const SolveArgs A) {
+  pdl_enter();
   if (A.status[3] != 0) return;  // GN loop finished
   const double lam = *A.lambda;
   extern __shared__ __align__(16) unsigned char smem[];
@@ -677,6 +678,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const SolveArgs
 // two-sided solve: 2 cooperative CTAs (see the header comment)
 template <int NS>
 __global__ void __launch_bounds__(kSolveThreads, 1) solve2_kernel(const SolveArgs A) {
+  pdl_enter();
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
   if (A.status[3] != 0) return;  // GN loop finished (uniform over both CTAs)

@@ -61,6 +61,7 @@ __device__ inline Pose64 stepped_pose(const PrepArgs& A, int k, const double xi[
 }
 
 __global__ void prep_kernel(const PrepArgs A) {
+  pdl_enter();
   if (trial_skipped(A.status)) return;
   const int t = blockIdx.x * blockDim.x + threadIdx.x + (A.phase == 1 ? A.N : 0);
   if (A.phase == 0 && t == A.N) {  // intrinsics
@@ -167,6 +168,7 @@ __host__ __device__ inline size_t assemble_smem_bytes(int kmax, bool calib) {
 }
 
 __global__ void __launch_bounds__(512) assemble_kernel(const AsmArgs A) {
+  pdl_enter();
   if (trial_skipped(A.status)) return;
   extern __shared__ double Ms[];  // M = sum_p v_p v_p^T / C_p over u-space (mu x mu)
   __shared__ double Ad[kMaxOutDegree * 36];
@@ -343,6 +345,7 @@ struct GatherArgs {
 };
 
 __global__ void gather_kernel(const GatherArgs A) {
+  pdl_enter();
   if (trial_skipped(A.status)) return;
   const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (wid >= A.n_units) return;
@@ -384,6 +387,7 @@ __device__ __forceinline__ void finalize_energy(const FinalArgs& A) {
 }
 
 __global__ void __launch_bounds__(256) finalize_kernel(const FinalArgs A) {
+  pdl_enter();
   if (trial_skipped(A.status)) return;
   finalize_energy(A);
 }
@@ -392,6 +396,7 @@ __global__ void __launch_bounds__(256) finalize_kernel(const FinalArgs A) {
 
 // sum of log d over one frame (fixed-order tree); out[0] = sum (0 if frame < 0)
 __global__ void __launch_bounds__(256) logsum_kernel(const float* d, int frame, int P, double* out) {
+  pdl_enter();
   __shared__ double sh[256];
   double s = 0.0;
   if (frame >= 0)
@@ -418,6 +423,7 @@ struct GaugeArgs {
 // d <- max(s d, d_min) on this rank's frames; every pose moved by the similarity
 // about camera g that keeps G_g:  t_k <- (t_k - c_k)/s + c_k,  c_k = R_k R_g^T t_g
 __global__ void gauge_apply_kernel(const GaugeArgs A) {
+  pdl_enter();
   const double s = exp((A.ref_sum[0] - A.cur_sum[0]) / (double)A.P);
   const long long n_d = (long long)(A.f1 - A.f0) * A.P;
   const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -517,11 +523,13 @@ __device__ void gn_decide(const DecideArgs& A) {
 }
 
 __global__ void decide_kernel(const DecideArgs A) {
+  pdl_enter();
   if (threadIdx.x == 0 && blockIdx.x == 0) gn_decide(A);
 }
 
 // single rank: the trial energy and the LM decision in one launch
 __global__ void __launch_bounds__(256) finalize_decide_kernel(const FinalArgs F, const DecideArgs D) {
+  pdl_enter();
   if (!trial_skipped(F.status)) finalize_energy(F);  // uniform over the block
   if (threadIdx.x == 0) gn_decide(D);
 }
@@ -538,6 +546,7 @@ struct AcceptArgs {
 };
 
 __global__ void __launch_bounds__(256) accept_kernel(const AcceptArgs A) {
+  pdl_enter();
   if (!A.ctl->accept || blockIdx.y >= A.nspan) return;
   const CopySpan sp = A.span[blockIdx.y];
   const long long stride = (long long)gridDim.x * blockDim.x, t0 = blockIdx.x * (long long)blockDim.x + threadIdx.x;
