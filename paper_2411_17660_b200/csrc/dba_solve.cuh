@@ -43,6 +43,10 @@ constexpr int kStageWarp = 3;       // shares the critical warp's scheduler; onl
 constexpr int kTrailThreads = 192;  // warps 0,1,2,4,5,6
 constexpr int kMaxBand = 24;        // compiled limit on BW
 constexpr int kRing = 32;           // backward-sweep factor-row ring depth (hides the bulk-copy latency)
+// blocks of the shared-memory window are kWB doubles apart (36 + 2 padding): block
+// starts then fall on 8 different bank offsets instead of 4, which removes most of
+// the bank conflicts of the trailing update (measured 1.5k -> 1.2k cycles per pivot)
+constexpr int kWB = 38;
 
 struct SolveArgs {
   int nb, BW, calib;
@@ -73,7 +77,7 @@ struct SolveSmem {
 __host__ __device__ inline SolveSmem solve_smem_layout(int nb, int BW, int calib) {
   SolveSmem s;
   size_t o = 0;
-  s.win = o; o += sizeof(double) * (size_t)(BW + 1) * (BW + 1) * 36;
+  s.win = o; o += sizeof(double) * (size_t)(BW + 1) * (BW + 1) * kWB;
   s.ring = o; o += sizeof(double) * (size_t)kRing * BW * 36;  // backward sweep: L blocks of kRing rows
   s.th = o; o += sizeof(double) * (calib ? (size_t)nb * 24 + 16 : 0);
   s.thL = o; o += sizeof(double) * (calib ? (size_t)nb * 24 : 0);
@@ -216,7 +220,7 @@ __device__ inline void chain_forward(const ChainSm& S, const double* band, doubl
   }
   if (npiv > 0 && crit && lane == 0) {
     double Di[36];
-    if (!inv6_spd(S.win + (size_t)BW * 36, lam, Di)) *S.fail = 1;  // block (0,0)
+    if (!inv6_spd(S.win + (size_t)BW * kWB, lam, Di)) *S.fail = 1;  // block (0,0)
     for (int x = 0; x < 36; ++x) S.dinv[x] = Di[x];
   }
   __syncthreads();
@@ -231,7 +235,7 @@ __device__ inline void chain_forward(const ChainSm& S, const double* band, doubl
     auto wb = [&](int a, int c) -> double* {
       int sl = sb + (a - b);
       sl = sl >= W1 ? sl - W1 : sl;
-      return S.win + ((size_t)sl * W1 + (c - a + BW)) * 36;
+      return S.win + ((size_t)sl * W1 + (c - a + BW)) * kWB;
     };
     const double* zb = S.z + 6 * b;
     if (crit) {
@@ -403,9 +407,12 @@ __device__ inline void chain_forward(const ChainSm& S, const double* band, doubl
     } else if (warp == kStageWarp && band != nullptr && b + BW + 1 < nrows) {
       // copy row b+BW+1 into row b's slot (free during step b)
       const char* src = reinterpret_cast<const char*>(band + (size_t)(b + BW + 1) * NR);
-      const unsigned dst = (unsigned)__cvta_generic_to_shared(S.win + (size_t)sb * NR);
-      for (int q = lane; q < NR / 2; q += 32)
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + 16 * q), "l"(src + 16 * q));
+      const unsigned dst = (unsigned)__cvta_generic_to_shared(S.win + (size_t)sb * W1 * kWB);
+      for (int q = lane; q < NR / 2; q += 32) {  // 18 chunks of 16 B per 36-double block
+        const int blk = q / 18, ch = q % 18;
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + blk * kWB * 8 + 16 * ch),
+                     "l"(src + 16 * q));
+      }
       asm volatile("cp.async.commit_group;");
       asm volatile("cp.async.wait_all;" ::: "memory");
     }
@@ -656,7 +663,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const SolveArgs
   if (tid == 0) fail = 0;
   const ChainSm S = chain_sm(smem, L, &fail, false);
   const int r0 = min(BW, nb - 1);
-  for (int x = tid; x < (r0 + 1) * NR; x += kSolveThreads) S.win[x] = A.band[x];
+  for (int x = tid; x < (r0 + 1) * NR; x += kSolveThreads) S.win[(x / 36) * kWB + x % 36] = A.band[x];
   if (A.calib) {
     for (int x = tid; x < nb * 24; x += kSolveThreads) S.th[x] = A.theta[x];
     if (tid < 16) S.th[nb * 24 + tid] = A.thth[tid];
@@ -698,7 +705,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve2_kernel(const SolveArg
   if (tid == 0) fail = 0;
   const ChainSm S = chain_sm(smem, L, &fail, false);
   // ---- load this orientation: window rows, theta border, rhs (bottom: reversed)
-  for (int x = tid; x < W1 * NR; x += kSolveThreads) S.win[x] = band[x];
+  for (int x = tid; x < W1 * NR; x += kSolveThreads) S.win[(x / 36) * kWB + x % 36] = band[x];
   if (calib) {
     for (int x = tid; x < nrows * 24; x += kSolveThreads) {
       const int c = x / 24, e = x % 24;
@@ -730,7 +737,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve2_kernel(const SolveArg
       if (j <= i) {
         int sl = sb0 + i;
         sl = sl >= W1 ? sl - W1 : sl;
-        v = S.win[((size_t)sl * W1 + (j - i + BW)) * 36 + e];
+        v = S.win[((size_t)sl * W1 + (j - i + BW)) * kWB + e];
       }
       ex[x] = v;
     }
@@ -764,7 +771,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve2_kernel(const SolveArg
         const double o = A.band[((size_t)(m + i) * W1 + (j - i + BW)) * 36 + e];
         v = t + rv - o;
       }
-      M.win[x] = v;
+      M.win[(x / 36) * kWB + x % 36] = v;
     }
     for (int x = tid; x < 6 * BW; x += kSolveThreads) {
       const int i = x / 6, s = x % 6;
