@@ -988,11 +988,7 @@ int launch_solve(Ctx& c, int slot) {
   return cuda_status(cudaGetLastError());
 }
 
-int launch_decide(Ctx& c) {
-  dba_plan* p = c.p;
-  (void)p;
-  return launch(c, decide_kernel, dim3(1), dim3(32), 0, false, decide_args(c));
-}
+int launch_decide(Ctx& c) { return launch(c, decide_kernel, dim3(1), dim3(32), 0, false, decide_args(c)); }
 
 // accepted trial (slot 1) -> current iterate (slot 0)
 int launch_accept(Ctx& c) {
