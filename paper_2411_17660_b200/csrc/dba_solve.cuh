@@ -39,8 +39,8 @@ namespace dba {
 #endif
 constexpr int kSolveThreads = 256;
 constexpr int kCritWarp = 7;
-constexpr int kStageWarp = 3;       // shares the critical warp's scheduler; only issues cp.async
-constexpr int kTrailThreads = 192;  // warps 0,1,2,4,5,6
+constexpr int kStageWarp = 3;       // also a trailing warp; issues the next row's cp.async first
+constexpr int kTrailThreads = 224;  // warps 0..6
 constexpr int kMaxBand = 24;        // compiled limit on BW
 constexpr int kRing = 32;           // backward-sweep factor-row ring depth (hides the bulk-copy latency)
 // blocks of the shared-memory window are kWB doubles apart (36 + 2 padding): block
@@ -211,8 +211,8 @@ __device__ inline void chain_forward(const ChainSm& S, const double* band, doubl
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int W1 = BW + 1, NR = W1 * 36;
   const bool crit = warp == kCritWarp;
-  const bool trail = (warp & 3) != 3;
-  const int gt = (warp - (warp >> 2)) * 32 + lane;
+  const bool trail = !crit;
+  const int gt = tid;
   if (tid == 0) {
     int q = 0;
     for (int ao = 0; ao < BW; ++ao)
@@ -286,6 +286,18 @@ __device__ inline void chain_forward(const ChainSm& S, const double* band, doubl
       }
       for (int e = lane; e < 36; e += 32) Lband[((size_t)b * W1 + BW) * 36 + e] = Db[e];
     } else if (trail) {
+      const bool stage = warp == kStageWarp && band != nullptr && b + BW + 1 < nrows;
+      if (stage) {
+        // copy row b+BW+1 into row b's slot (free during step b)
+        const char* src = reinterpret_cast<const char*>(band + (size_t)(b + BW + 1) * NR);
+        const unsigned dst = (unsigned)__cvta_generic_to_shared(S.win + (size_t)sb * W1 * kWB);
+        for (int q = lane; q < NR / 2; q += 32) {  // 18 chunks of 16 B per 36-double block
+          const int blk = q / 18, ch = q % 18;
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + blk * kWB * 8 + 16 * ch),
+                       "l"(src + 16 * q));
+        }
+        asm volatile("cp.async.commit_group;");
+      }
       // panels L_ab = S_ab D_b^-1 (a in (b, amax]), L_tb = S_tb D_b^-1
       const int prow = 6 * na + (calib ? 4 : 0);
       for (int x = gt; x < prow; x += kTrailThreads) {
@@ -404,17 +416,7 @@ __device__ inline void chain_forward(const ChainSm& S, const double* band, doubl
         }
       }
       if (calib && gt < 24) S.thL[(size_t)b * 24 + gt] = S.tbuf[gt];  // L_tb for the backward sweep
-    } else if (warp == kStageWarp && band != nullptr && b + BW + 1 < nrows) {
-      // copy row b+BW+1 into row b's slot (free during step b)
-      const char* src = reinterpret_cast<const char*>(band + (size_t)(b + BW + 1) * NR);
-      const unsigned dst = (unsigned)__cvta_generic_to_shared(S.win + (size_t)sb * W1 * kWB);
-      for (int q = lane; q < NR / 2; q += 32) {  // 18 chunks of 16 B per 36-double block
-        const int blk = q / 18, ch = q % 18;
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + blk * kWB * 8 + 16 * ch),
-                     "l"(src + 16 * q));
-      }
-      asm volatile("cp.async.commit_group;");
-      asm volatile("cp.async.wait_all;" ::: "memory");
+      if (stage) asm volatile("cp.async.wait_all;" ::: "memory");
     }
 #ifdef DBA_SOLVE_PROF
     __syncwarp();
