@@ -178,10 +178,13 @@ int dba_build_system(dba_plan* plan, const dba_options* opt, const dba_buffers* 
  * stream and accumulates their durations (resolved at each stream sync). */
 typedef struct {
   int64_t launches;        /* all kernels launched by the library */
-  int64_t pass_launches;   /* fused linearise/back-substitute passes */
+  int64_t pass_launches;   /* fused linearising passes (system build) */
   int64_t solve_launches;  /* reduced-system factorisations */
   double pass_ms;          /* summed CUDA-event time of the pass launches */
   double solve_ms;         /* summed CUDA-event time of the solve launches */
+  int64_t pass_runs;       /* pass launches that ran (the rest were gated off by a rejection) */
+  int64_t energy_launches; /* energy-only trial passes (back-substitution + residuals) */
+  double energy_ms;        /* summed CUDA-event time of the energy-only passes */
 } dba_stats;
 
 int dba_plan_set_profiling(dba_plan* plan, int32_t enable);

@@ -80,6 +80,7 @@ class Stats(ctypes.Structure):
     _fields_ = [
         ("launches", ctypes.c_int64), ("pass_launches", ctypes.c_int64),
         ("solve_launches", ctypes.c_int64), ("pass_ms", c_dbl), ("solve_ms", c_dbl),
+        ("pass_runs", ctypes.c_int64), ("energy_launches", ctypes.c_int64), ("energy_ms", c_dbl),
     ]
 
 

@@ -1,0 +1,209 @@
+// Energy-only trial pass: back-substitution at x_c and the Eq. 3 (+ Eq. 4) energy at
+// the trial state x_n, without Jacobians of x_n, per-edge Hessians or the Schur
+// fill-in.  The LM controller only needs the trial energy to accept or reject; the
+// full pass (pass_kernel) then linearises an ACCEPTED trial, so a rejected trial
+// costs one solve plus this kernel.
+//
+// One thread per source-frame pixel, a CTA per 256-pixel tile of one frame: the
+// thread walks the frame's out-edges twice (flow records re-read from L1), first
+// for delta d_p = (g_d,p - sum_e E_e,p . delta_e) / C_p (the
+// same terms as pass_kernel phase A), then for the residual energy at
+// (x_n, d_n).  No shared-memory pixel staging and no block barriers inside the
+// pixel loop.  Per-CTA partial energies (float64, fixed-order tree) are summed by
+// finalize in CTA order, so every energy the controller compares (including the
+// initial one) comes from this kernel with one summation order.
+#pragma once
+
+#include "dba_pass.cuh"
+
+namespace dba {
+
+constexpr int kEnergyThreads = 256;
+
+struct EnergyArgs {
+  int H, W, P, tiles;  // tiles = ceil(P / 256) per frame
+  int kmax;
+  int backsub, freeze;
+  const int* status;
+  const int* csr_off;
+  const int* slot_flow;
+  const int* frame_of;
+  const EdgeLin* lin;
+  const EdgeBack* back;
+  const float4* flow;
+  const float* d_cur;
+  float* d_new;
+  const float* prior;
+  const uint8_t* pmask;
+  const float* pweight;
+  float alpha, eta, d_min;
+  const double* intr_c;
+  const double* intr_n;
+  int gauge_frame;
+  const double* gstate_c;
+  double* part;  // (NL * tiles) per-CTA energies
+};
+
+// flow records of the thread's pixel are kept in shared memory between the two
+// walks when the frame's out-degree allows (else re-read through L1)
+constexpr int kEnergyStageMax = 16;
+
+__host__ __device__ inline size_t energy_smem_bytes(int kmax) {
+  const size_t k = (size_t)(kmax > 0 ? kmax : 1);
+  const size_t stage = kmax <= kEnergyStageMax ? sizeof(float4) * kEnergyThreads * k : 0;
+  return stage + (sizeof(EdgeLin) + sizeof(EdgeBack) + sizeof(float4*)) * k;
+}
+
+// pix_terms with the hardware reciprocal (rcp.approx, <= 1 ulp): the energy walk
+// only needs the residual and validity
+__device__ __forceinline__ PixTerms pix_terms_e(const EdgeLin& e, float qx, float qy, float d, float fx, float fy,
+                                                float cx, float cy, float Wf, float Hf, const float4& fw) {
+  PixTerms o;
+  const float X = fmaf(e.R[0], qx, fmaf(e.R[1], qy, e.R[2])) + e.t[0] * d;
+  const float Y = fmaf(e.R[3], qx, fmaf(e.R[4], qy, e.R[5])) + e.t[1] * d;
+  const float Z = fmaf(e.R[6], qx, fmaf(e.R[7], qy, e.R[8])) + e.t[2] * d;
+  bool ok = Z > 1e-4f * d;
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(Z));
+  o.iz = ok ? r : 0.f;
+  o.xt = X * o.iz;
+  o.yt = Y * o.iz;
+  const float pu = fmaf(fx, o.xt, cx), pv = fmaf(fy, o.yt, cy);
+  ok = ok && pu >= -1e-9f && pu <= Wf + 1e-9f && pv >= -1e-9f && pv <= Hf + 1e-9f;
+  o.ok = ok;
+  o.wu = ok ? fw.z : 0.f;
+  o.wv = ok ? fw.w : 0.f;
+  o.ru = ok ? fw.x - pu : 0.f;
+  o.rv = ok ? fw.y - pv : 0.f;
+  return o;
+}
+
+template <bool CALIB>
+__global__ void __launch_bounds__(kEnergyThreads) energy_kernel(const EnergyArgs A) {
+  pdl_enter();
+  if (trial_skipped(A.status)) return;
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ double red[kEnergyThreads / 32];
+  __shared__ double kappa_s;
+  const int fl = blockIdx.x / A.tiles, tile = blockIdx.x % A.tiles;
+  const int s0 = A.csr_off[fl], k = A.csr_off[fl + 1] - s0;
+  const int f = A.frame_of[fl];
+  const bool stage = A.kmax <= kEnergyStageMax;
+  float4* fs = reinterpret_cast<float4*>(smem);  // [k][256] when staged
+  EdgeLin* sl = reinterpret_cast<EdgeLin*>(smem + (stage ? sizeof(float4) * kEnergyThreads * A.kmax : 0));
+  EdgeBack* sb = reinterpret_cast<EdgeBack*>(sl + k);
+  const float4** fp0 = reinterpret_cast<const float4**>(sb + k);
+  const int tid = threadIdx.x;
+  const bool phaseA = A.backsub && !A.freeze;
+  const int P = A.P;
+  for (int x = tid; x < k * (int)(sizeof(EdgeLin) / 16); x += kEnergyThreads)
+    reinterpret_cast<float4*>(sl)[x] = reinterpret_cast<const float4*>(A.lin + s0)[x];
+  if (phaseA)
+    for (int x = tid; x < k * (int)(sizeof(EdgeBack) / 16); x += kEnergyThreads)
+      reinterpret_cast<float4*>(sb)[x] = reinterpret_cast<const float4*>(A.back + s0)[x];
+  for (int x = tid; x < k; x += kEnergyThreads) fp0[x] = A.flow + (size_t)A.slot_flow[s0 + x] * P;
+  __syncthreads();
+  const bool gauge = phaseA && f == A.gauge_frame && k > 0;
+  if (gauge && tid == 0) {  // A5: kappa = (rho - h . delta_local) / gamma, as pass_kernel
+    const double* gs = A.gstate_c;
+    double hd = 0.0;
+    for (int a = 0; a < k; ++a)
+      for (int q = 0; q < 6; ++q) hd += gs[2 + 6 * a + q] * (double)sb[a].dlt[q];
+    if (CALIB)
+      for (int q = 0; q < 4; ++q) hd += gs[2 + 6 * k + q] * (A.intr_n[q] - A.intr_c[q]);
+    kappa_s = (gs[1] - hd) / gs[0];
+  }
+  __syncthreads();
+
+  const int p = tile * kEnergyThreads + tid;
+  const bool in = p < P;
+  const int pc = in ? p : 0;  // clamped: out-of-range lanes read pixel 0 and contribute nothing
+  const float Wf = (float)A.W, Hf = (float)A.H;
+  const float fxn = (float)A.intr_n[0], fyn = (float)A.intr_n[1];
+  const float cxn = (float)A.intr_n[2], cyn = (float)A.intr_n[3];
+  const float pu = (float)(pc % A.W), pv = (float)(pc / A.W);
+  const size_t fpx = (size_t)f * P + pc;
+  const float dc = A.d_cur[fpx];
+  float dn = dc;
+  float ap = 0.f;
+  if (A.prior != nullptr) ap = A.alpha * (A.pweight ? A.pweight[f] : 1.f) * (float)A.pmask[fpx];
+  if (phaseA) {
+    const float fxc = (float)A.intr_c[0], fyc = (float)A.intr_c[1];
+    const float cxc = (float)A.intr_c[2], cyc = (float)A.intr_c[3];
+    const float dth[4] = {(float)(A.intr_n[0] - A.intr_c[0]), (float)(A.intr_n[1] - A.intr_c[1]),
+                          (float)(A.intr_n[2] - A.intr_c[2]), (float)(A.intr_n[3] - A.intr_c[3])};
+    const float qx = (pu - cxc) / fxc, qy = (pv - cyc) / fyc;
+    float Cp = 0.f, gdp = 0.f, accp = 0.f;
+    float4 fnext = k > 0 ? __ldg(fp0[0] + pc) : make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int a = 0; a < k; ++a) {
+      const float4 fw = fnext;
+      if (a + 1 < k) fnext = __ldg(fp0[a + 1] + pc);  // one edge ahead
+      if (stage) fs[a * kEnergyThreads + tid] = fw;
+      const EdgeBack& e = sb[a];
+      const PixTerms T = pix_terms_e(reinterpret_cast<const EdgeLin&>(e), qx, qy, dc, fxc, fyc, cxc, cyc, Wf, Hf, fw);
+      const float fxi = fxc * T.iz, fyi = fyc * T.iz;
+      const float Jdu = fxi * (e.t[0] - T.xt * e.t[2]);
+      const float Jdv = fyi * (e.t[1] - T.yt * e.t[2]);
+      const float* dl = e.dlt;
+      float ju = fxi * dc * (dl[0] - T.xt * dl[2]) +
+                 fxc * (-T.xt * T.yt * dl[3] + (1.f + T.xt * T.xt) * dl[4] - T.yt * dl[5]);
+      float jv = fyi * dc * (dl[1] - T.yt * dl[2]) +
+                 fyc * (-(1.f + T.yt * T.yt) * dl[3] + T.xt * T.yt * dl[4] + T.xt * dl[5]);
+      if (CALIB) {
+        const float cu0 = T.iz * (e.R[0] - T.xt * e.R[6]), cu1 = T.iz * (e.R[1] - T.xt * e.R[7]);
+        const float cv0 = T.iz * (e.R[3] - T.yt * e.R[6]), cv1 = T.iz * (e.R[4] - T.yt * e.R[7]);
+        ju += (T.xt - cu0 * qx) * dth[0] + (-cu1 * qy * fxc / fyc) * dth[1] + (1.f - cu0) * dth[2] +
+              (-cu1 * fxc / fyc) * dth[3];
+        jv += (-cv0 * qx * fyc / fxc) * dth[0] + (T.yt - cv1 * qy) * dth[1] + (-cv0 * fyc / fxc) * dth[2] +
+              (1.f - cv1) * dth[3];
+      }
+      const float au = T.wu * Jdu, av = T.wv * Jdv;
+      Cp += fmaf(au, Jdu, av * Jdv);
+      gdp += fmaf(au, T.ru, av * T.rv);
+      accp += fmaf(au, ju, av * jv);
+    }
+    float C = A.eta + Cp, gd = gdp;
+    if (A.prior != nullptr) {
+      C += ap;
+      gd += ap * (A.prior[fpx] - dc);
+    }
+    float dd = (gd - accp) / C;
+    if (gauge) dd -= (float)(kappa_s / (double)dc);  // A5: r/C - kappa/d
+    dn = fmaxf(dc + dd, A.d_min);
+  }
+  if (in) A.d_new[fpx] = dn;
+  // residual energy at (x_n, d_n)
+  const float qx = (pu - cxn) / fxn, qy = (pv - cyn) / fyn;
+  float en = 0.f;
+  const bool have = phaseA && stage;  // records staged by the first walk
+  float4 fnext = (!have && k > 0) ? __ldg(fp0[0] + pc) : make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int a = 0; a < k; ++a) {
+    float4 fw;
+    if (have) {
+      fw = fs[a * kEnergyThreads + tid];
+    } else {
+      fw = fnext;
+      if (a + 1 < k) fnext = __ldg(fp0[a + 1] + pc);
+    }
+    const PixTerms T = pix_terms_e(sl[a], qx, qy, dn, fxn, fyn, cxn, cyn, Wf, Hf, fw);
+    en += T.wu * T.ru * T.ru + T.wv * T.rv * T.rv;
+  }
+  double ed = in ? (double)en : 0.0;
+  if (A.prior != nullptr && in) {
+    const float dd = A.prior[fpx] - dn;
+    ed += (double)(ap * dd * dd);
+  }
+  // fixed-order block reduction
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) ed += __shfl_xor_sync(0xffffffffu, ed, off);
+  if ((tid & 31) == 0) red[tid >> 5] = ed;
+  __syncthreads();
+  if (tid == 0) {
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < kEnergyThreads / 32; ++w) s += red[w];
+    A.part[blockIdx.x] = s;
+  }
+}
+
+}  // namespace dba

@@ -23,6 +23,7 @@
 
 #include "../../include/dba_b200.h"
 #include "dba_common.cuh"
+#include "dba_energy.cuh"
 #include "dba_pass.cuh"
 #include "dba_solve.cuh"
 #include "dba_system.cuh"
@@ -64,9 +65,11 @@ inline size_t align_up(size_t x) { return (x + kAlign - 1) & ~(kAlign - 1); }
 
 struct Readback {
   int status[4];  // flags word, see trial_skipped (dba_common.cuh)
+  int gate[4];    // flags word of the accepted-trial linearisation (gn_decide)
   double cond;
   double energy;
-  double pad[2];
+  unsigned long long runs;  // gated system passes that ran (profiling)
+  double pad;
 };
 
 struct Layout {
@@ -76,7 +79,7 @@ struct Layout {
   size_t off_F, off_f, units, contrib, meta_end;
   // state
   size_t poses[2], intr[2], disps[2], xi, delta, lin, back, adj;
-  size_t part_edge, part_M, part_w, part_frame, Fbuf, sys[2], gstate[2], Lband, rLband, mid, flags, ctl, gauge, total;
+  size_t part_edge, part_M, part_w, part_frame, part_energy, Fbuf, sys[2], gstate[2], Lband, rLband, mid, flags, ctl, gauge, total;
 };
 
 }  // namespace
@@ -104,9 +107,9 @@ struct dba_plan {
     bool on = false;
     std::vector<cudaEvent_t> pool;
     int used = 0;
-    std::vector<std::pair<int, int>> pass_ev, solve_ev;
-    long long launches = 0, pass_launches = 0, solve_launches = 0;
-    double pass_ms = 0.0, solve_ms = 0.0;
+    std::vector<std::pair<int, int>> pass_ev, solve_ev, energy_ev;
+    long long launches = 0, pass_launches = 0, solve_launches = 0, pass_runs = 0, energy_launches = 0;
+    double pass_ms = 0.0, solve_ms = 0.0, energy_ms = 0.0;
     // DBA_TIMELINE=1 (diagnostic): an event after every launch; per-label time from the
     // previous event (kernel + launch gap), printed at each resolve
     bool timeline = false;
@@ -561,6 +564,7 @@ int dba_plan_create(const dba_problem_desc* d, dba_plan** out) {
   L.part_M = take(sizeof(double) * n_pM);
   L.part_w = take(sizeof(double) * n_pw);
   L.part_frame = take(sizeof(double) * kFrameVals * (size_t)p->nseg);
+  L.part_energy = take(sizeof(double) * (size_t)std::max(p->NL, 1) * ((p->P + kEnergyThreads - 1) / kEnergyThreads));
   L.Fbuf = take(sizeof(double) * nF);
   L.Lband = take(sizeof(double) * std::max<long long>(p->band_len, 1));
   L.rLband = take(sizeof(double) * (p->two_sided ? p->band_len : 1));
@@ -721,8 +725,13 @@ void prof_resolve(dba_plan* p) {
     float ms = 0.f;
     if (cudaEventElapsedTime(&ms, pr.pool[e.first], pr.pool[e.second]) == cudaSuccess) pr.solve_ms += ms;
   }
+  for (auto& e : pr.energy_ev) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, pr.pool[e.first], pr.pool[e.second]) == cudaSuccess) pr.energy_ms += ms;
+  }
   pr.pass_ev.clear();
   pr.solve_ev.clear();
+  pr.energy_ev.clear();
   pr.used = 0;
 }
 
@@ -777,6 +786,8 @@ int launch_prep(Ctx& c, int cur, int nxt, bool init) {
   a.lin = c.at<EdgeLin>(p->L.lin);
   a.back = c.at<EdgeBack>(p->L.back);
   a.adj = c.at<double>(p->L.adj);
+  a.slot_edge = c.at<int>(p->L.slot_edge);
+  a.bad_edge = c.at<int>(p->L.flags) + 1;
   // phase 0: one thread per pose (exp-map retraction) + intrinsics; phase 1: one per
   // edge slot (relative poses, adjoints) reading phase 0's poses; one warp per block
   // spreads the fp64 work over the SMs
@@ -801,16 +812,24 @@ int launch_pass_t(Ctx& c, const PassArgs& a) {
     DBA_CUDA(cudaEventRecord(pr.pool[ev.first], c.st));
   }
   if (int s = launch(c, k, dim3(c.p->G), dim3(kPassThreads), c.p->pass_smem, false, a)) return s;
-  mark(c, "pass");
-  pr.pass_launches++;
+  mark(c, a.system ? "pass" : "pass-E");
+  if (a.system) {
+    pr.pass_launches++;
+    if (!a.runs) pr.pass_runs++;  // gated launches count on the device
+  } else {
+    pr.energy_launches++;
+  }
   if (pr.on) {
     DBA_CUDA(cudaEventRecord(pr.pool[ev.second], c.st));
-    pr.pass_ev.push_back(ev);
+    (a.system ? pr.pass_ev : pr.energy_ev).push_back(ev);
   }
   return cuda_status(cudaGetLastError());
 }
 
-int launch_pass(Ctx& c, int cur, int nxt, bool backsub, bool system) {
+int* gate_word(Ctx& c) { return c.at<Readback>(c.p->L.flags)->gate; }
+
+// gated: skipped unless the LM controller accepted the trial (Readback::gate)
+int launch_pass(Ctx& c, int cur, int nxt, bool backsub, bool system, bool gated = false) {
   dba_plan* p = c.p;
   if (p->NL == 0) return DBA_OK;
   PassArgs a;
@@ -822,7 +841,8 @@ int launch_pass(Ctx& c, int cur, int nxt, bool backsub, bool system) {
   a.backsub = backsub ? 1 : 0;
   a.system = system ? 1 : 0;
   a.stage = p->stage;
-  a.status = c.at<int>(p->L.flags);
+  a.status = gated ? gate_word(c) : c.at<int>(p->L.flags);
+  a.runs = gated ? &c.at<Readback>(p->L.flags)->runs : nullptr;
   a.csr_off = c.at<int>(p->L.csr_off);
   a.slot_flow = c.at<int>(p->L.slot_flow);
   a.frame_of = c.at<int>(p->L.frame_of);
@@ -867,23 +887,113 @@ DecideArgs decide_args(Ctx& c) {
   a.lam_max = c.o->lambda_max;
   a.cond_max = c.o->calib_cond_max;
   a.status = c.at<int>(p->L.flags);
+  a.gate = gate_word(c);
   a.cond = &c.at<Readback>(p->L.flags)->cond;
   a.energy = c.at<double>(p->L.sys[1]) + p->energy_off;
   a.ctl = c.at<Control>(p->L.ctl);
   return a;
 }
 
+// energy-only trial pass (energy_kernel): d_n by back-substitution at x_c (when
+// `backsub`) and the energy at x_n, partials in part_energy
+int launch_epass(Ctx& c, int cur, int nxt, bool backsub) {
+  dba_plan* p = c.p;
+  if (p->NL == 0) return DBA_OK;
+  EnergyArgs a;
+  a.H = p->H;
+  a.W = p->W;
+  a.P = p->P;
+  a.tiles = (p->P + kEnergyThreads - 1) / kEnergyThreads;
+  a.kmax = std::max(p->kmax, 1);
+  a.backsub = backsub ? 1 : 0;
+  a.freeze = p->freeze_d;
+  a.status = c.at<int>(p->L.flags);
+  a.csr_off = c.at<int>(p->L.csr_off);
+  a.slot_flow = c.at<int>(p->L.slot_flow);
+  a.frame_of = c.at<int>(p->L.frame_of);
+  a.lin = c.at<EdgeLin>(p->L.lin);
+  a.back = c.at<EdgeBack>(p->L.back);
+  a.flow = reinterpret_cast<const float4*>(c.b->flow);
+  a.d_cur = c.at<float>(p->L.disps[cur]);
+  a.d_new = c.at<float>(p->L.disps[nxt]);
+  a.prior = p->prior ? c.b->prior : nullptr;
+  a.pmask = p->prior ? c.b->prior_mask : nullptr;
+  a.pweight = p->prior ? c.b->prior_weight : nullptr;
+  a.alpha = (float)c.o->alpha;
+  a.eta = (float)c.o->eta;
+  a.d_min = (float)c.o->d_min;
+  a.intr_c = c.at<double>(p->L.intr[cur]);
+  a.intr_n = c.at<double>(p->L.intr[nxt]);
+  a.gauge_frame = p->gauge_on ? p->gauge_frame : -1;
+  a.gstate_c = c.at<double>(p->L.gstate[cur]);
+  a.part = c.at<double>(p->L.part_energy);
+  const size_t smem = energy_smem_bytes(a.kmax);
+  auto k = p->calib ? energy_kernel<true> : energy_kernel<false>;
+  DBA_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  auto& pr = p->prof;
+  std::pair<int, int> ev{-1, -1};
+  if (pr.on) {
+    if (int s = ev_pair(c, ev)) return s;
+    DBA_CUDA(cudaEventRecord(pr.pool[ev.first], c.st));
+  }
+  if (int s = launch(c, k, dim3(p->NL * a.tiles), dim3(kEnergyThreads), smem, false, a)) return s;
+  mark(c, "pass-E");
+  pr.energy_launches++;
+  if (pr.on) {
+    DBA_CUDA(cudaEventRecord(pr.pool[ev.second], c.st));
+    pr.energy_ev.push_back(ev);
+  }
+  return DBA_OK;
+}
+
 int launch_decide(Ctx& c);
 
-// assemble -> gather -> finalize [-> all-reduce]; with `decide` the LM decision on
-// the resulting trial energy follows (fused into finalize on a single rank)
-int launch_system(Ctx& c, int slot, bool decide = false) {
+// finalize the energy of `slot` [-> all-reduce of the energy and the bad-edge flag];
+// with `decide` the LM decision follows (fused into finalize on a single rank)
+int launch_energy(Ctx& c, int slot, bool decide, int* status, bool from_epass = false) {
   dba_plan* p = c.p;
+  FinalArgs f;
+  f.status = status;
+  if (from_epass) {  // per-CTA partials of energy_kernel
+    f.n = p->NL * ((p->P + kEnergyThreads - 1) / kEnergyThreads);
+    f.stride = 1;
+    f.part_frame = c.at<double>(p->L.part_energy);
+  } else {  // per-segment partials of pass_kernel
+    f.n = p->nseg;
+    f.stride = kFrameVals;
+    f.part_frame = c.at<double>(p->L.part_frame);
+  }
+  f.energy_out = c.at<double>(p->L.sys[slot]) + p->energy_off;
+  const bool multi = c.comm && p->nranks > 1;
+  if (decide && !multi) {
+    if (int s = launch(c, finalize_decide_kernel, dim3(1), dim3(256), 0, false, f, decide_args(c))) return s;
+    mark(c, "fin+decide");
+    return DBA_OK;
+  }
+  if (int s = launch(c, finalize_kernel, dim3(1), dim3(256), 0, false, f)) return s;
+  mark(c, "finalize");
+  if (multi) {
+    if (!nccl().ok) return DBA_ENCCL;
+    double* e = c.at<double>(p->L.sys[slot]) + p->energy_off;
+    if (nccl().AllReduce(e, e, 1, ncclDouble, ncclSum, c.comm, c.st) != ncclSuccess) return DBA_ENCCL;
+    int* bad = c.at<int>(p->L.flags) + 1;
+    if (nccl().AllReduce(bad, bad, 1, ncclInt32, ncclMin, c.comm, c.st) != ncclSuccess) return DBA_ENCCL;
+  }
+  if (decide) return launch_decide(c);
+  return DBA_OK;
+}
+
+// assemble -> gather -> [all-reduce of the system] -> energy (launch_energy).  The
+// energy is reduced on its own so that trial energies (energy-only passes) and
+// system energies are summed identically across ranks.
+int launch_system(Ctx& c, int slot, bool decide = false, bool gated = false) {
+  dba_plan* p = c.p;
+  int* status = gated ? gate_word(c) : c.at<int>(p->L.flags);
   if (p->NL > 0) {
     AsmArgs a;
     a.calib = p->calib;
     a.nve = p->nve;
-    a.status = c.at<int>(p->L.flags);
+    a.status = status;
     a.csr_off = c.at<int>(p->L.csr_off);
     a.slot_edge = c.at<int>(p->L.slot_edge);
     a.frame_seg = c.at<int>(p->L.frame_seg);
@@ -905,43 +1015,27 @@ int launch_system(Ctx& c, int slot, bool decide = false) {
     const size_t smem = assemble_smem_bytes(std::max(p->kmax, 1), p->calib);
     DBA_CUDA(cudaFuncSetAttribute(assemble_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     if (int s = launch(c, assemble_kernel, dim3(p->NL), dim3(512), smem, false, a)) return s;
-  mark(c, "assemble");
+    mark(c, "assemble");
   }
   if (p->n_units > 0) {
     GatherArgs g;
     g.n_units = p->n_units;
-    g.status = c.at<int>(p->L.flags);
+    g.status = status;
     g.units = c.at<GatherUnit>(p->L.units);
     g.contrib = c.at<Contrib>(p->L.contrib);
     g.Fbuf = c.at<double>(p->L.Fbuf);
     g.sys = c.at<double>(p->L.sys[slot]);
     const int threads = 256, warps = threads / 32;
     if (int s = launch(c, gather_kernel, dim3((p->n_units + warps - 1) / warps), dim3(threads), 0, false, g)) return s;
-  mark(c, "gather");
+    mark(c, "gather");
   }
-  FinalArgs f;
-  f.n = p->nseg;
-  f.status = c.at<int>(p->L.flags);
-  f.part_frame = c.at<double>(p->L.part_frame);
-  f.energy_out = c.at<double>(p->L.sys[slot]) + p->energy_off;
-  const bool multi = c.comm && p->nranks > 1;
-  if (decide && !multi) {
-    if (int s = launch(c, finalize_decide_kernel, dim3(1), dim3(256), 0, false, f, decide_args(c))) return s;
-  mark(c, "fin+decide");
-    return DBA_OK;
-  }
-  if (int s = launch(c, finalize_kernel, dim3(1), dim3(256), 0, false, f)) return s;
-  mark(c, "finalize");
-  if (multi) {
+  if (c.comm && p->nranks > 1) {
     if (!nccl().ok) return DBA_ENCCL;
-    double* s = c.at<double>(p->L.sys[slot]);
-    if (nccl().AllReduce(s, s, (size_t)p->sys_len, ncclDouble, ncclSum, c.comm, c.st) != ncclSuccess)
+    double* sy = c.at<double>(p->L.sys[slot]);
+    if (nccl().AllReduce(sy, sy, (size_t)p->energy_off, ncclDouble, ncclSum, c.comm, c.st) != ncclSuccess)
       return DBA_ENCCL;
-    int* bad = c.at<int>(p->L.flags) + 1;
-    if (nccl().AllReduce(bad, bad, 1, ncclInt32, ncclMin, c.comm, c.st) != ncclSuccess) return DBA_ENCCL;
   }
-  if (decide) return launch_decide(c);
-  return DBA_OK;
+  return launch_energy(c, slot, decide, status);
 }
 
 int launch_solve(Ctx& c, int slot) {
@@ -1060,7 +1154,10 @@ int initial_pass(Ctx& c) {
   if (s) return s;
   if ((s = launch_prep(c, 0, 0, true))) return s;
   if ((s = launch_pass(c, 0, 0, false, true))) return s;
-  return launch_system(c, 0);
+  if ((s = launch_system(c, 0))) return s;
+  // the energy the controller starts from, summed like every trial energy
+  if ((s = launch_epass(c, 0, 0, false))) return s;
+  return launch_energy(c, 0, false, c.at<int>(p->L.flags), true);
 }
 
 int gauge_sum(Ctx& c, const float* d, double* out) {
@@ -1111,10 +1208,16 @@ int dba_solve(dba_plan* p, const dba_options* o, const dba_buffers* b, dba_repor
   for (int seen = 0; o->iters > 0;) {
     const int batch = std::max(1, o->iters - seen);
     for (int t = 0; t < batch; ++t) {
+      // trial: solve, step, energy-only pass (back-substitution + residuals at x_n),
+      // decision; only an accepted trial that continues the loop is linearised
+      // (the same pass with the system, gated on the decision) -- rejected trials
+      // cost no Jacobians or Schur fill-in
       if ((s = launch_solve(c, 0))) return rep->status = s;
       if ((s = launch_prep(c, 0, 1, false))) return rep->status = s;
-      if ((s = launch_pass(c, 0, 1, true, true))) return rep->status = s;
-      if ((s = launch_system(c, 1, true))) return rep->status = s;
+      if ((s = launch_epass(c, 0, 1, true))) return rep->status = s;
+      if ((s = launch_energy(c, 1, true, c.at<int>(p->L.flags), true))) return rep->status = s;
+      if ((s = launch_pass(c, 1, 1, false, true, true))) return rep->status = s;
+      if ((s = launch_system(c, 1, false, true))) return rep->status = s;
       if ((s = launch_accept(c))) return rep->status = s;
     }
     DBA_CUDA(cudaMemcpyAsync(p->ctl_h, c.at<Control>(p->L.ctl), sizeof(Control), cudaMemcpyDeviceToHost, c.st));
@@ -1169,8 +1272,14 @@ int dba_solve(dba_plan* p, const dba_options* o, const dba_buffers* b, dba_repor
       return rep->status = s;
     DBA_CUDA(cudaMemcpyAsync(&rep->scale, gsum + 2, sizeof(double), cudaMemcpyDeviceToHost, c.st));
   }
+  if (p->prof.on)
+    DBA_CUDA(cudaMemcpyAsync(&p->rb->runs, &c.at<Readback>(p->L.flags)->runs, sizeof(unsigned long long),
+                             cudaMemcpyDeviceToHost, c.st));
   DBA_CUDA(cudaStreamSynchronize(c.st));
-  if (p->prof.on) prof_resolve(p);
+  if (p->prof.on) {
+    p->prof.pass_runs += (long long)p->rb->runs;
+    prof_resolve(p);
+  }
   rep->status = DBA_OK;
   return DBA_OK;
 }
@@ -1189,9 +1298,13 @@ int dba_plan_get_stats(dba_plan* p, dba_stats* st, int32_t reset) {
   st->solve_launches = p->prof.solve_launches;
   st->pass_ms = p->prof.pass_ms;
   st->solve_ms = p->prof.solve_ms;
+  st->pass_runs = p->prof.pass_runs;
+  st->energy_launches = p->prof.energy_launches;
+  st->energy_ms = p->prof.energy_ms;
   if (reset) {
     p->prof.launches = p->prof.pass_launches = p->prof.solve_launches = 0;
-    p->prof.pass_ms = p->prof.solve_ms = 0.0;
+    p->prof.pass_runs = p->prof.energy_launches = 0;
+    p->prof.pass_ms = p->prof.solve_ms = p->prof.energy_ms = 0.0;
   }
   return DBA_OK;
 }

@@ -50,6 +50,7 @@ struct PassArgs {
   int system;   // produce system partials (0: energy only)
   int stage;    // flow records of the next sub-tile are staged in smem with cp.async
   const int* status;  // see trial_skipped
+  unsigned long long* runs;  // counts executed launches (profiling of gated passes) or null
   const int* csr_off;
   const int* slot_flow;
   const int* frame_of;
@@ -186,6 +187,7 @@ template <bool CALIB>
 __global__ void __launch_bounds__(kPassThreads, 1) pass_kernel(const PassArgs A) {
   pdl_enter();
   if (trial_skipped(A.status)) return;
+  if (A.runs && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(A.runs, 1ull);
   extern __shared__ __align__(16) unsigned char smem[];
   constexpr int NVE = kEdgeVals + (CALIB ? kCalibVals : 0);
   const PassSmem L = pass_smem_layout(A.kmax, CALIB, A.stage != 0);

@@ -276,6 +276,9 @@ __device__ inline void chain_forward(const ChainSm& S, const double* band, doubl
           if (h1) S11[e1] = d1;
         }
         __syncwarp();
+#ifdef DBA_SOLVE_PROF
+        const long long pc1 = clock64();
+#endif
         if (lane == 0 && b + 1 < npiv) {
           double Di[36];
           if (!inv6_spd(S11, lam, Di)) *S.fail = 1;
@@ -283,6 +286,13 @@ __device__ inline void chain_forward(const ChainSm& S, const double* band, doubl
 #pragma unroll
           for (int x = 0; x < 36; ++x) Dnx[x] = Di[x];
         }
+#ifdef DBA_SOLVE_PROF
+        __syncwarp();
+        if (blockIdx.x == 0 && lane == 0) {
+          g_prof[8] += pc1 - pt0;
+          g_prof[9] += clock64() - pc1;
+        }
+#endif
       }
       for (int e = lane; e < 36; e += 32) Lband[((size_t)b * W1 + BW) * 36 + e] = Db[e];
     } else if (trail) {

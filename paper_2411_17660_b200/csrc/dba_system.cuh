@@ -35,6 +35,8 @@ struct PrepArgs {
   EdgeLin* lin;
   EdgeBack* back;
   double* adj;  // (EL,36) Ad(G_ij) at x_n
+  const int* slot_edge;
+  int* bad_edge;  // smallest edge whose x_n constants are non-finite (flags word [1])
 };
 
 __device__ inline void clamped_xi(const PrepArgs& A, int k, double xi[6]) {
@@ -113,6 +115,13 @@ __global__ void prep_kernel(const PrepArgs A) {
       eb.dlt[r] = (float)s2;
     }
     eb.pad[0] = eb.pad[1] = 0.f;
+    // a non-finite trial pose or intrinsics: the energy-only trial pass cannot see it
+    // (invalid projections contribute zero), so flag the edge here
+    bool ok = true;
+    for (int c = 0; c < 9; ++c) ok = ok && isfinite(Rn[c]);
+    for (int c = 0; c < 3; ++c) ok = ok && isfinite(gn.t[c]);
+    for (int c = 0; c < 4; ++c) ok = ok && isfinite(A.intr_n[c]);
+    if (!ok && A.bad_edge) atomicMin(A.bad_edge, A.slot_edge[s]);
     A.lin[s] = el;
     A.back[s] = eb;
     for (int c = 0; c < 36; ++c) A.adj[36 * (size_t)s + c] = An[c];
@@ -366,7 +375,8 @@ __global__ void gather_kernel(const GatherArgs A) {
 // ---------------------------------------------------------------- finalize
 
 struct FinalArgs {
-  int n;  // number of frame-partial rows (segments)
+  int n;       // number of partial rows (pass segments or energy CTAs)
+  int stride;  // doubles between rows; the energy is the first value of a row
   const int* status;
   const double* part_frame;
   double* energy_out;
@@ -376,7 +386,7 @@ struct FinalArgs {
 __device__ __forceinline__ void finalize_energy(const FinalArgs& A) {
   __shared__ double sh[256];
   double s = 0.0;
-  for (int x = threadIdx.x; x < A.n; x += 256) s += A.part_frame[(long long)x * kFrameVals];
+  for (int x = threadIdx.x; x < A.n; x += 256) s += A.part_frame[(long long)x * A.stride];
   sh[threadIdx.x] = s;
   __syncthreads();
   for (int off = 128; off >= 1; off >>= 1) {
@@ -465,6 +475,7 @@ struct DecideArgs {
   int iters, calib;
   double lam_min, lam_max, cond_max;
   int* status;          // flags word
+  int* gate;            // flags word of the kernels that linearise an accepted trial
   double* cond;         // theta pivot ratio of the last solve
   const double* energy; // energy of the trial state (slot 1)
   Control* ctl;
@@ -515,6 +526,10 @@ __device__ void gn_decide(const DecideArgs& A) {
     }
   }
   c->done = done;
+  if (A.gate) {  // [0]: rejected, [3]: finished -> trial_skipped
+    A.gate[0] = !c->accept;
+    A.gate[3] = done;
+  }
   st[0] = 0;
   st[1] = INT_MAX;
   st[2] = 0;

@@ -317,7 +317,8 @@ class DBASolver:
         _raise_for(self.lib.dba_plan_get_stats(self._plan, ctypes.byref(st), int(bool(reset))))
         return {"launches": st.launches, "pass_launches": st.pass_launches,
                 "solve_launches": st.solve_launches, "pass_ms": st.pass_ms,
-                "solve_ms": st.solve_ms}
+                "solve_ms": st.solve_ms, "pass_runs": st.pass_runs,
+                "energy_launches": st.energy_launches, "energy_ms": st.energy_ms}
 
     def debug_trial(self, poses, disps, intr, flow, prior=None, prior_mask=None, *, lam=1e-4,
                     **opts):
