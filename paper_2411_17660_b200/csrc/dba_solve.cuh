@@ -47,6 +47,10 @@ constexpr int kRing = 32;           // backward-sweep factor-row ring depth (hid
 // starts then fall on 8 different bank offsets instead of 4, which removes most of
 // the bank conflicts of the trailing update (measured 1.5k -> 1.2k cycles per pivot)
 constexpr int kWB = 38;
+#ifndef DBA_KTR
+#define DBA_KTR 3
+#endif
+constexpr int kTR = DBA_KTR;  // rows of a trailing-update output block per thread
 
 struct SolveArgs {
   int nb, BW, calib;
@@ -203,8 +207,22 @@ struct ChainSm {
 // diagonal block includes the critical warp's update).  ncols: offset of the theta
 // rows in th / z.  Writes factor rows [0, nrows) to Lband (off-diagonal L blocks) and
 // D_b^-1 to the diagonal slot of rows [0, npiv).
-#ifdef DBA_SOLVE_PROF
+#if defined(DBA_SOLVE_PROF) || defined(DBA_CRIT_PROF)
 __device__ long long g_prof[16];  // [role*2 + {work, barrier wait}] cycles, CTA 0
+#endif
+// DBA_CRIT_PROF: phase clock of the critical warp (CTA 0, lane 0) in registers, one
+// global write at the end (g_prof[8..12]: L, S11 update, inversion, export, barrier)
+#ifdef DBA_CRIT_PROF
+#define CRIT_MARK(i)                   \
+  do {                                 \
+    const long long t_ = clock64();    \
+    cpa[i] += t_ - cpt;                \
+    cpt = t_;                          \
+  } while (0)
+#else
+#define CRIT_MARK(i) \
+  do {               \
+  } while (0)
 #endif
 __device__ inline void chain_forward(const ChainSm& S, const double* band, double* Lband, int nrows, int npiv,
                                      int BW, int calib, int ncols, double lam) {
@@ -224,8 +242,13 @@ __device__ inline void chain_forward(const ChainSm& S, const double* band, doubl
     for (int x = 0; x < 36; ++x) S.dinv[x] = Di[x];
   }
   __syncthreads();
+#ifdef DBA_CRIT_PROF
+  long long cpa[5] = {0, 0, 0, 0, 0}, cpt = clock64();
+#endif
   int sb = 0;  // slot of block row b (= b % W1)
-  for (int b = 0; b < npiv && !*S.fail; ++b) {
+  // a failed pivot sets *S.fail; the sweep runs on (values are discarded) so the
+  // loop needs no per-step flag read
+  for (int b = 0; b < npiv; ++b) {
 #ifdef DBA_SOLVE_PROF
     const long long pt0 = clock64();
 #endif
@@ -241,44 +264,36 @@ __device__ inline void chain_forward(const ChainSm& S, const double* band, doubl
     if (crit) {
       // next pivot: L_{b+1,b} = S_{b+1,b} D_b^-1, S_{b+1,b+1} -= L S^T, D_{b+1}^-1
       if (na > 0) {
+        // lane r < 6 owns row r: L_{b+1,b}[r] = S1[r] D_b^-1, then S11[r] -= L[r] S1^T
+        // and z_{b+1}[r] -= L[r] z_b, without exchanging L between lanes (operand
+        // blocks are broadcast loads)
         const double* S1 = wb(b + 1, b);
         double* S11 = wb(b + 1, b + 1);
-        double* Lr = S.cbuf;
-        const int e0 = lane, e1 = lane + 32;
-        const bool h1 = e1 < 36;
-        const int r0 = e0 / 6, c0 = e0 % 6, r1 = h1 ? e1 / 6 : 0, c1 = h1 ? e1 % 6 : 0;
-        {
-          double s0 = 0.0, s1 = 0.0;
+        if (lane < 6) {
+          const int r = lane;
+          double Lr[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
 #pragma unroll
           for (int k = 0; k < 6; ++k) {
-            s0 = fma(S1[6 * r0 + k], Db[6 * k + c0], s0);
-            s1 = fma(S1[6 * r1 + k], Db[6 * k + c1], s1);
+            const double sk = S1[6 * r + k];
+#pragma unroll
+            for (int c = 0; c < 6; ++c) Lr[c] = fma(sk, Db[6 * k + c], Lr[c]);
           }
-          Lr[e0] = s0;
-          if (h1) Lr[e1] = s1;
-        }
-        __syncwarp();
-        {
-          double d0 = S11[e0], d1 = h1 ? S11[e1] : 0.0;
+          double d[6], zs = S.z[6 * (b + 1) + r];
+#pragma unroll
+          for (int c = 0; c < 6; ++c) d[c] = S11[6 * r + c];
 #pragma unroll
           for (int k = 0; k < 6; ++k) {
-            d0 = fma(-Lr[6 * r0 + k], S1[6 * c0 + k], d0);
-            d1 = fma(-Lr[6 * r1 + k], S1[6 * c1 + k], d1);
-          }
-          if (lane < 6) {
-            double s = S.z[6 * (b + 1) + lane];
 #pragma unroll
-            for (int k = 0; k < 6; ++k) s = fma(-Lr[6 * lane + k], zb[k], s);
-            S.z[6 * (b + 1) + lane] = s;
+            for (int c = 0; c < 6; ++c) d[c] = fma(-Lr[k], S1[6 * c + k], d[c]);
+            zs = fma(-Lr[k], zb[k], zs);
           }
-          __syncwarp();
-          S11[e0] = d0;  // keep the updated block (non-pivot rows are exported from here)
-          if (h1) S11[e1] = d1;
+#pragma unroll
+          for (int c = 0; c < 6; ++c) S11[6 * r + c] = d[c];  // non-pivot rows are exported from here
+          S.z[6 * (b + 1) + r] = zs;
         }
+        CRIT_MARK(0);
         __syncwarp();
-#ifdef DBA_SOLVE_PROF
-        const long long pc1 = clock64();
-#endif
+        CRIT_MARK(1);
         if (lane == 0 && b + 1 < npiv) {
           double Di[36];
           if (!inv6_spd(S11, lam, Di)) *S.fail = 1;
@@ -286,17 +301,16 @@ __device__ inline void chain_forward(const ChainSm& S, const double* band, doubl
 #pragma unroll
           for (int x = 0; x < 36; ++x) Dnx[x] = Di[x];
         }
-#ifdef DBA_SOLVE_PROF
         __syncwarp();
-        if (blockIdx.x == 0 && lane == 0) {
-          g_prof[8] += pc1 - pt0;
-          g_prof[9] += clock64() - pc1;
-        }
-#endif
+        CRIT_MARK(2);
       }
-      for (int e = lane; e < 36; e += 32) Lband[((size_t)b * W1 + BW) * 36 + e] = Db[e];
+      CRIT_MARK(3);
     } else if (trail) {
+#ifdef DBA_SOLVE_NOSTAGE
+      const bool stage = false;  // timing experiment (results invalid)
+#else
       const bool stage = warp == kStageWarp && band != nullptr && b + BW + 1 < nrows;
+#endif
       if (stage) {
         // copy row b+BW+1 into row b's slot (free during step b)
         const char* src = reinterpret_cast<const char*>(band + (size_t)(b + BW + 1) * NR);
@@ -308,6 +322,9 @@ __device__ inline void chain_forward(const ChainSm& S, const double* band, doubl
         }
         asm volatile("cp.async.commit_group;");
       }
+      // D_b^-1 -> the diagonal slot of factor row b (threads past the panel rows)
+      if (gt >= kTrailThreads - 64 && gt < kTrailThreads - 28)
+        Lband[((size_t)b * W1 + BW) * 36 + (gt - (kTrailThreads - 64))] = Db[gt - (kTrailThreads - 64)];
       // panels L_ab = S_ab D_b^-1 (a in (b, amax]), L_tb = S_tb D_b^-1
       const int prow = 6 * na + (calib ? 4 : 0);
       for (int x = gt; x < prow; x += kTrailThreads) {
@@ -340,27 +357,31 @@ __device__ inline void chain_forward(const ChainSm& S, const double* band, doubl
 #endif
       // trailing update S_ac -= L_ab S_cb^T (except (b+1,b+1)), border, rhs
       const int npair = na * (na + 1) / 2;
-      const int n1 = npair * 3;
+      const int n1 = npair * (6 / kTR);
       const int n2 = calib ? na * 4 : 0;
       const int n3 = calib ? 4 : 0;
       const int n4 = 6 * (na > 0 ? na - 1 : 0) + (calib ? 4 : 0);
+#ifdef DBA_SOLVE_NOTRAIL
+      const int ntot = 0;  // timing experiment: critical warp without the trailing traffic
+#else
       const int ntot = n1 + n2 + n3 + n4;
+#endif
       for (int x = gt; x < ntot; x += kTrailThreads) {
         if (x < n1) {
-          const int pidx = x / 3, rr = 2 * (x % 3);
+          const int pidx = x / (6 / kTR), rr = kTR * (x % (6 / kTR));
           if (pidx == 0) continue;  // (b+1, b+1): critical warp
           const short2 pr = S.pairs[pidx];
           const int a = b + 1 + pr.x, cc = b + 1 + pr.y;
           const double* La = S.pbuf + 36 * pr.x + 6 * rr;
           const double2* Sc = reinterpret_cast<const double2*>(wb(cc, b));
           double2* O = reinterpret_cast<double2*>(wb(a, cc) + 6 * rr);
-          double ar[2][6], o[2][6];
+          double ar[kTR][6], o[kTR][6];
 #pragma unroll
-          for (int r = 0; r < 2; ++r)
+          for (int r = 0; r < kTR; ++r)
 #pragma unroll
             for (int d = 0; d < 6; ++d) ar[r][d] = La[6 * r + d];
 #pragma unroll
-          for (int q = 0; q < 6; ++q) {
+          for (int q = 0; q < 3 * kTR; ++q) {
             const double2 v = O[q];
             o[(2 * q) / 6][(2 * q) % 6] = v.x;
             o[(2 * q + 1) / 6][(2 * q + 1) % 6] = v.y;
@@ -375,12 +396,12 @@ __device__ inline void chain_forward(const ChainSm& S, const double* band, doubl
               sc[2 * q + 1] = v.y;
             }
 #pragma unroll
-            for (int r = 0; r < 2; ++r)
+            for (int r = 0; r < kTR; ++r)
 #pragma unroll
               for (int d = 0; d < 6; ++d) o[r][c] = fma(-ar[r][d], sc[d], o[r][c]);
           }
 #pragma unroll
-          for (int q = 0; q < 6; ++q)
+          for (int q = 0; q < 3 * kTR; ++q)
             O[q] = make_double2(o[(2 * q) / 6][(2 * q) % 6], o[(2 * q + 1) / 6][(2 * q + 1) % 6]);
         } else if (x < n1 + n2) {
           const int y2 = x - n1, co = y2 / 4, tt = y2 % 4;
@@ -441,8 +462,13 @@ __device__ inline void chain_forward(const ChainSm& S, const double* band, doubl
       g_prof[2 * role + 1] += pt2 - pt1;
     }
 #endif
+    if (crit) CRIT_MARK(4);
     sb = (sb + 1 == W1) ? 0 : sb + 1;
   }
+#ifdef DBA_CRIT_PROF
+  if (crit && lane == 0 && blockIdx.x == 0)
+    for (int i = 0; i < 5; ++i) g_prof[8 + i] += cpa[i];
+#endif
 }
 
 // theta block (4x4 Schur complement + lam): Cholesky, forward+backward solve in
