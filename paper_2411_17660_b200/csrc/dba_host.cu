@@ -891,6 +891,11 @@ DecideArgs decide_args(Ctx& c) {
   a.cond = &c.at<Readback>(p->L.flags)->cond;
   a.energy = c.at<double>(p->L.sys[1]) + p->energy_off;
   a.ctl = c.at<Control>(p->L.ctl);
+  a.poses_dst = c.at<double>(p->L.poses[0]);
+  a.poses_src = c.at<double>(p->L.poses[1]);
+  a.pose_words = 7 * p->N;
+  a.intr_dst = c.at<double>(p->L.intr[0]);
+  a.intr_src = c.at<double>(p->L.intr[1]);
   return a;
 }
 
@@ -1035,6 +1040,8 @@ int launch_system(Ctx& c, int slot, bool decide = false, bool gated = false) {
     if (nccl().AllReduce(sy, sy, (size_t)p->energy_off, ncclDouble, ncclSum, c.comm, c.st) != ncclSuccess)
       return DBA_ENCCL;
   }
+  // an accepted trial's energy is already known (energy_kernel)
+  if (gated) return DBA_OK;
   return launch_energy(c, slot, decide, status);
 }
 
@@ -1082,27 +1089,7 @@ int launch_solve(Ctx& c, int slot) {
   return cuda_status(cudaGetLastError());
 }
 
-int launch_decide(Ctx& c) { return launch(c, decide_kernel, dim3(1), dim3(32), 0, false, decide_args(c)); }
-
-// accepted trial (slot 1) -> current iterate (slot 0)
-int launch_accept(Ctx& c) {
-  dba_plan* p = c.p;
-  AcceptArgs a;
-  a.ctl = c.at<Control>(p->L.ctl);
-  a.nspan = 0;
-  auto span = [&](size_t dst, size_t src, long long words) {
-    a.span[a.nspan++] = CopySpan{c.at<float>(dst), c.at<float>(src), words};
-  };
-  span(p->L.poses[0], p->L.poses[1], 14LL * p->N);
-  span(p->L.intr[0], p->L.intr[1], 8);
-  span(p->L.disps[0] + sizeof(float) * (size_t)p->f0 * p->P, p->L.disps[1] + sizeof(float) * (size_t)p->f0 * p->P,
-       (long long)p->NL * p->P);
-  span(p->L.sys[0], p->L.sys[1], 2 * p->sys_len);
-  span(p->L.gstate[0], p->L.gstate[1], 2LL * (6 * kMaxOutDegree + 8));
-  if (int s = launch(c, accept_kernel, dim3(2 * std::max(p->G, 1), a.nspan), dim3(256), 0, false, a)) return s;
-  mark(c, "accept");
-  return DBA_OK;
-}
+int launch_decide(Ctx& c) { return launch(c, decide_kernel, dim3(1), dim3(256), 0, false, decide_args(c)); }
 
 int upload_control(Ctx& c, double lam, double Ec) {
   Control h{};
@@ -1216,9 +1203,10 @@ int dba_solve(dba_plan* p, const dba_options* o, const dba_buffers* b, dba_repor
       if ((s = launch_prep(c, 0, 1, false))) return rep->status = s;
       if ((s = launch_epass(c, 0, 1, true))) return rep->status = s;
       if ((s = launch_energy(c, 1, true, c.at<int>(p->L.flags), true))) return rep->status = s;
-      if ((s = launch_pass(c, 1, 1, false, true, true))) return rep->status = s;
-      if ((s = launch_system(c, 1, false, true))) return rep->status = s;
-      if ((s = launch_accept(c))) return rep->status = s;
+      // accepted and continuing: linearise at the trial state straight into slot 0
+      // (disparities d_n of slot 1 -> slot 0, system and gauge state of slot 0)
+      if ((s = launch_pass(c, 1, 0, false, true, true))) return rep->status = s;
+      if ((s = launch_system(c, 0, false, true))) return rep->status = s;
     }
     DBA_CUDA(cudaMemcpyAsync(p->ctl_h, c.at<Control>(p->L.ctl), sizeof(Control), cudaMemcpyDeviceToHost, c.st));
     DBA_CUDA(cudaStreamSynchronize(c.st));
@@ -1239,7 +1227,10 @@ int dba_solve(dba_plan* p, const dba_options* o, const dba_buffers* b, dba_repor
   }
   rep->converged = ctl.converged;
   const int it = ctl.it;
-  const int cur = 0;
+  // poses/intrinsics of an accepted trial are copied to slot 0 by the decision; its
+  // disparities reach slot 0 only through the linearisation, which the final
+  // accepted trial skips
+  const int cur = 0, dcur = ctl.accept ? 1 : 0;
   Ec = ctl.Ec;
   const double lam = ctl.lam;
   rep->iterations = it;
@@ -1251,7 +1242,7 @@ int dba_solve(dba_plan* p, const dba_options* o, const dba_buffers* b, dba_repor
   DBA_CUDA(cudaMemcpyAsync(b->intr_out, c.at<double>(p->L.intr[cur]), sizeof(double) * 4,
                            cudaMemcpyDeviceToDevice, c.st));
   if (p->NL > 0)
-    DBA_CUDA(cudaMemcpyAsync(b->disps_out + (size_t)p->f0 * p->P, c.at<float>(p->L.disps[cur]) + (size_t)p->f0 * p->P,
+    DBA_CUDA(cudaMemcpyAsync(b->disps_out + (size_t)p->f0 * p->P, c.at<float>(p->L.disps[dcur]) + (size_t)p->f0 * p->P,
                              sizeof(float) * (size_t)p->P * p->NL, cudaMemcpyDeviceToDevice, c.st));
   if (p->gauge_on) {
     if ((s = gauge_sum(c, b->disps_out, gsum + 1))) return rep->status = s;

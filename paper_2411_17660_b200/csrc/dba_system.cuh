@@ -386,6 +386,7 @@ struct FinalArgs {
 __device__ __forceinline__ void finalize_energy(const FinalArgs& A) {
   __shared__ double sh[256];
   double s = 0.0;
+#pragma unroll 8
   for (int x = threadIdx.x; x < A.n; x += 256) s += A.part_frame[(long long)x * A.stride];
   sh[threadIdx.x] = s;
   __syncthreads();
@@ -461,8 +462,10 @@ namespace dba {
 // ---------------------------------------------------------------- GN controller
 // The Levenberg-Marquardt schedule (A1) runs on the device so that a
 // whole solve is enqueued without host round trips: state slot 0 is the current
-// iterate, slot 1 the trial; decide_kernel accepts / rejects and accept_kernel
-// copies an accepted trial over the current iterate.
+// iterate, slot 1 the trial; the decision (finalize_decide_kernel, or decide_kernel
+// after the all-reduce) copies accepted poses/intrinsics to slot 0, and the gated
+// linearisation of an accepted trial writes slot 0's disparities, system and gauge
+// state.
 constexpr int kTraceMax = 64;  // == DBA_TRACE_MAX
 
 struct Control {
@@ -479,6 +482,14 @@ struct DecideArgs {
   double* cond;         // theta pivot ratio of the last solve
   const double* energy; // energy of the trial state (slot 1)
   Control* ctl;
+  // acceptance: the trial poses / intrinsics (slot 1) become the iterate (slot 0);
+  // disparities, system and gauge state are written to slot 0 by the gated
+  // linearisation of the accepted trial
+  double* poses_dst;
+  const double* poses_src;
+  int pose_words;
+  double* intr_dst;
+  const double* intr_src;
 };
 
 __device__ void gn_decide(const DecideArgs& A) {
@@ -537,40 +548,31 @@ __device__ void gn_decide(const DecideArgs& A) {
   *A.cond = 0.0;
 }
 
+// the LM decision (thread 0) and, on acceptance, the pose/intrinsics copy by the
+// whole block
+__device__ void decide_block(const DecideArgs& A) {
+  __shared__ int acc;
+  if (threadIdx.x == 0) {
+    gn_decide(A);
+    acc = A.ctl->accept;
+  }
+  __syncthreads();
+  if (acc) {
+    for (int x = threadIdx.x; x < A.pose_words; x += blockDim.x) A.poses_dst[x] = A.poses_src[x];
+    if (threadIdx.x < 4) A.intr_dst[threadIdx.x] = A.intr_src[threadIdx.x];
+  }
+}
+
 __global__ void decide_kernel(const DecideArgs A) {
   pdl_enter();
-  if (threadIdx.x == 0 && blockIdx.x == 0) gn_decide(A);
+  decide_block(A);
 }
 
 // single rank: the trial energy and the LM decision in one launch
 __global__ void __launch_bounds__(256) finalize_decide_kernel(const FinalArgs F, const DecideArgs D) {
   pdl_enter();
   if (!trial_skipped(F.status)) finalize_energy(F);  // uniform over the block
-  if (threadIdx.x == 0) gn_decide(D);
-}
-
-struct CopySpan {
-  float* dst;
-  const float* src;
-  long long n;  // 4-byte words
-};
-struct AcceptArgs {
-  const Control* ctl;
-  CopySpan span[5];
-  int nspan;
-};
-
-__global__ void __launch_bounds__(256) accept_kernel(const AcceptArgs A) {
-  pdl_enter();
-  if (!A.ctl->accept || blockIdx.y >= A.nspan) return;
-  const CopySpan sp = A.span[blockIdx.y];
-  const long long stride = (long long)gridDim.x * blockDim.x, t0 = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  const bool vec = ((reinterpret_cast<uintptr_t>(sp.dst) | reinterpret_cast<uintptr_t>(sp.src)) & 15) == 0;
-  long long n4 = vec ? sp.n / 4 : 0;
-#pragma unroll 4
-  for (long long x = t0; x < n4; x += stride)
-    reinterpret_cast<float4*>(sp.dst)[x] = reinterpret_cast<const float4*>(sp.src)[x];
-  for (long long x = 4 * n4 + t0; x < sp.n; x += stride) sp.dst[x] = sp.src[x];
+  decide_block(D);
 }
 
 }  // namespace dba
