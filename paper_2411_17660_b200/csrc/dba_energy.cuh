@@ -5,7 +5,7 @@
 // costs one solve plus this kernel.
 //
 // One thread per source-frame pixel, a CTA per 256-pixel tile of one frame: the
-// thread walks the frame's out-edges twice (flow records re-read from L1), first
+// thread walks the frame's out-edges twice (flow records staged in shared memory), first
 // for delta d_p = (g_d,p - sum_e E_e,p . delta_e) / C_p (the
 // same terms as pass_kernel phase A), then for the residual energy at
 // (x_n, d_n).  No shared-memory pixel staging and no block barriers inside the
@@ -44,8 +44,8 @@ struct EnergyArgs {
   double* part;  // (NL * tiles) per-CTA energies
 };
 
-// flow records of the thread's pixel are kept in shared memory between the two
-// walks when the frame's out-degree allows (else re-read through L1)
+// flow records of the thread's pixel are staged in shared memory (cp.async, one
+// burst per CTA) when the frame's out-degree allows (else both walks read through L1)
 constexpr int kEnergyStageMax = 16;
 
 __host__ __device__ inline size_t energy_smem_bytes(int kmax) {
@@ -118,6 +118,16 @@ __global__ void __launch_bounds__(kEnergyThreads) energy_kernel(const EnergyArgs
   const int p = tile * kEnergyThreads + tid;
   const bool in = p < P;
   const int pc = in ? p : 0;  // clamped: out-of-range lanes read pixel 0 and contribute nothing
+  // the thread's k flow records -> shared memory in one burst (each thread reads back
+  // only its own, so no barrier); without staging both walks read through L1
+  if (stage) {
+    for (int a = 0; a < k; ++a) {
+      const unsigned dst = (unsigned)__cvta_generic_to_shared(fs + a * kEnergyThreads + tid);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(fp0[a] + pc));
+    }
+    asm volatile("cp.async.commit_group;");
+  }
+  auto record = [&](int a) -> float4 { return stage ? fs[a * kEnergyThreads + tid] : __ldg(fp0[a] + pc); };
   const float Wf = (float)A.W, Hf = (float)A.H;
   const float fxn = (float)A.intr_n[0], fyn = (float)A.intr_n[1];
   const float cxn = (float)A.intr_n[2], cyn = (float)A.intr_n[3];
@@ -127,6 +137,7 @@ __global__ void __launch_bounds__(kEnergyThreads) energy_kernel(const EnergyArgs
   float dn = dc;
   float ap = 0.f;
   if (A.prior != nullptr) ap = A.alpha * (A.pweight ? A.pweight[f] : 1.f) * (float)A.pmask[fpx];
+  if (stage) asm volatile("cp.async.wait_all;" ::: "memory");
   if (phaseA) {
     const float fxc = (float)A.intr_c[0], fyc = (float)A.intr_c[1];
     const float cxc = (float)A.intr_c[2], cyc = (float)A.intr_c[3];
@@ -134,11 +145,8 @@ __global__ void __launch_bounds__(kEnergyThreads) energy_kernel(const EnergyArgs
                           (float)(A.intr_n[2] - A.intr_c[2]), (float)(A.intr_n[3] - A.intr_c[3])};
     const float qx = (pu - cxc) / fxc, qy = (pv - cyc) / fyc;
     float Cp = 0.f, gdp = 0.f, accp = 0.f;
-    float4 fnext = k > 0 ? __ldg(fp0[0] + pc) : make_float4(0.f, 0.f, 0.f, 0.f);
     for (int a = 0; a < k; ++a) {
-      const float4 fw = fnext;
-      if (a + 1 < k) fnext = __ldg(fp0[a + 1] + pc);  // one edge ahead
-      if (stage) fs[a * kEnergyThreads + tid] = fw;
+      const float4 fw = record(a);
       const EdgeBack& e = sb[a];
       const PixTerms T = pix_terms_e(reinterpret_cast<const EdgeLin&>(e), qx, qy, dc, fxc, fyc, cxc, cyc, Wf, Hf, fw);
       const float fxi = fxc * T.iz, fyi = fyc * T.iz;
@@ -175,16 +183,8 @@ __global__ void __launch_bounds__(kEnergyThreads) energy_kernel(const EnergyArgs
   // residual energy at (x_n, d_n)
   const float qx = (pu - cxn) / fxn, qy = (pv - cyn) / fyn;
   float en = 0.f;
-  const bool have = phaseA && stage;  // records staged by the first walk
-  float4 fnext = (!have && k > 0) ? __ldg(fp0[0] + pc) : make_float4(0.f, 0.f, 0.f, 0.f);
   for (int a = 0; a < k; ++a) {
-    float4 fw;
-    if (have) {
-      fw = fs[a * kEnergyThreads + tid];
-    } else {
-      fw = fnext;
-      if (a + 1 < k) fnext = __ldg(fp0[a + 1] + pc);
-    }
+    const float4 fw = record(a);
     const PixTerms T = pix_terms_e(sl[a], qx, qy, dn, fxn, fyn, cxn, cyn, Wf, Hf, fw);
     en += T.wu * T.ru * T.ru + T.wv * T.rv * T.rv;
   }

@@ -62,10 +62,13 @@ const NcclApi& nccl() {
 
 constexpr size_t kAlign = 256;
 inline size_t align_up(size_t x) { return (x + kAlign - 1) & ~(kAlign - 1); }
+inline long long align_doubles(long long n) { return (long long)(align_up(sizeof(double) * (size_t)n) / sizeof(double)); }
 
 struct Readback {
   int status[4];  // flags word, see trial_skipped (dba_common.cuh)
   int gate[4];    // flags word of the accepted-trial linearisation (gn_decide)
+  int spec[kMaxSpec - 1][4];  // flags words of damping candidates 1.. (gn_decide)
+  double spec_cond[kMaxSpec - 1];
   double cond;
   double energy;
   unsigned long long runs;  // gated system passes that ran (profiling)
@@ -91,6 +94,8 @@ struct dba_plan {
   int n_tiles = 0, G = 0, nseg = 0, n_units = 0, nve = kEdgeVals, stage = 1;
   size_t pass_smem = 0, solve_smem = 0;
   long long sys_len = 0;  // doubles in one packed reduced system
+  long long spec_delta = 0, spec_Lband = 0, spec_rLband = 0, spec_mid = 0;  // per damping candidate
+  int nspec = kMaxSpec;  // damping candidates solved per round by dba_solve
   long long band_len = 0, rband_off = 0, theta_off = 0, thth_off = 0, y_off = 0, energy_off = 0;
   int two_sided = 0, m_top = 0;  // two-CTA solve: pivots of the top chain
   std::vector<int> fixed_ridx;
@@ -556,7 +561,8 @@ int dba_plan_create(const dba_problem_desc* d, dba_plan** out) {
     L.gstate[s] = take(sizeof(double) * (6 * kMaxOutDegree + 8));
   }
   L.xi = take(sizeof(double) * 6 * N);
-  L.delta = take(sizeof(double) * (p->n_red + 4));
+  p->spec_delta = align_doubles(p->n_red + 4);
+  L.delta = take(sizeof(double) * p->spec_delta * kMaxSpec);
   L.lin = take(sizeof(EdgeLin) * p->EL);
   L.back = take(sizeof(EdgeBack) * p->EL);
   L.adj = take(sizeof(double) * 36 * (size_t)p->EL);
@@ -566,9 +572,13 @@ int dba_plan_create(const dba_problem_desc* d, dba_plan** out) {
   L.part_frame = take(sizeof(double) * kFrameVals * (size_t)p->nseg);
   L.part_energy = take(sizeof(double) * (size_t)std::max(p->NL, 1) * ((p->P + kEnergyThreads - 1) / kEnergyThreads));
   L.Fbuf = take(sizeof(double) * nF);
-  L.Lband = take(sizeof(double) * std::max<long long>(p->band_len, 1));
-  L.rLband = take(sizeof(double) * (p->two_sided ? p->band_len : 1));
-  L.mid = take(sizeof(double) * (p->two_sided ? solve_mid_len(p->BW) : 1));
+  // factor rows / exchange scratch per damping candidate
+  p->spec_Lband = align_doubles(std::max<long long>(p->band_len, 1));
+  p->spec_rLband = align_doubles(p->two_sided ? p->band_len : 1);
+  p->spec_mid = align_doubles(p->two_sided ? solve_mid_len(p->BW) : 1);
+  L.Lband = take(sizeof(double) * p->spec_Lband * kMaxSpec);
+  L.rLband = take(sizeof(double) * p->spec_rLband * kMaxSpec);
+  L.mid = take(sizeof(double) * p->spec_mid * kMaxSpec);
   L.flags = take(sizeof(Readback));
   L.ctl = take(sizeof(Control));
   L.gauge = take(sizeof(double) * 4);
@@ -764,7 +774,18 @@ int prepare(Ctx& c) {
   return DBA_OK;
 }
 
-int launch_prep(Ctx& c, int cur, int nxt, bool init) {
+int* gate_word(Ctx& c) { return c.at<Readback>(c.p->L.flags)->gate; }
+// flags word / condition slot of damping candidate k (0: the loop's own word)
+int* cand_flags(Ctx& c, int k) {
+  Readback* r = c.at<Readback>(c.p->L.flags);
+  return k == 0 ? r->status : r->spec[k - 1];
+}
+double* cand_cond(Ctx& c, int k) {
+  Readback* r = c.at<Readback>(c.p->L.flags);
+  return k == 0 ? &r->cond : &r->spec_cond[k - 1];
+}
+
+int launch_prep(Ctx& c, int cur, int nxt, bool init, int cand = 0) {
   dba_plan* p = c.p;
   PrepArgs a;
   a.N = p->N;
@@ -773,7 +794,7 @@ int launch_prep(Ctx& c, int cur, int nxt, bool init) {
   a.calib = p->calib;
   a.theta_off = 6 * p->nb;
   a.tmax = c.o->tangent_max;
-  a.status = c.at<int>(p->L.flags);
+  a.status = cand_flags(c, cand);
   a.ridx = c.at<int>(p->L.ridx);
   a.slot_i = c.at<int>(p->L.slot_i);
   a.slot_j = c.at<int>(p->L.slot_j);
@@ -781,13 +802,13 @@ int launch_prep(Ctx& c, int cur, int nxt, bool init) {
   a.poses_n = c.at<double>(p->L.poses[nxt]);
   a.intr_c = c.at<double>(p->L.intr[cur]);
   a.intr_n = c.at<double>(p->L.intr[nxt]);
-  a.delta = c.at<double>(p->L.delta);
+  a.delta = c.at<double>(p->L.delta) + cand * p->spec_delta;
   a.xi_out = c.at<double>(p->L.xi);
   a.lin = c.at<EdgeLin>(p->L.lin);
   a.back = c.at<EdgeBack>(p->L.back);
   a.adj = c.at<double>(p->L.adj);
   a.slot_edge = c.at<int>(p->L.slot_edge);
-  a.bad_edge = c.at<int>(p->L.flags) + 1;
+  a.bad_edge = cand_flags(c, cand) + 1;
   // phase 0: one thread per pose (exp-map retraction) + intrinsics; phase 1: one per
   // edge slot (relative poses, adjoints) reading phase 0's poses; one warp per block
   // spreads the fp64 work over the SMs
@@ -826,7 +847,6 @@ int launch_pass_t(Ctx& c, const PassArgs& a) {
   return cuda_status(cudaGetLastError());
 }
 
-int* gate_word(Ctx& c) { return c.at<Readback>(c.p->L.flags)->gate; }
 
 // gated: skipped unless the LM controller accepted the trial (Readback::gate)
 int launch_pass(Ctx& c, int cur, int nxt, bool backsub, bool system, bool gated = false) {
@@ -878,7 +898,7 @@ int launch_pass(Ctx& c, int cur, int nxt, bool backsub, bool system, bool gated 
 }
 
 // LM controller inputs: the trial (slot 1) energy, the flags word and the options
-DecideArgs decide_args(Ctx& c) {
+DecideArgs decide_args(Ctx& c, int cand = 0) {
   dba_plan* p = c.p;
   DecideArgs a;
   a.iters = c.o->iters;
@@ -886,9 +906,11 @@ DecideArgs decide_args(Ctx& c) {
   a.lam_min = c.o->lambda_min;
   a.lam_max = c.o->lambda_max;
   a.cond_max = c.o->calib_cond_max;
-  a.status = c.at<int>(p->L.flags);
+  a.status = cand_flags(c, cand);
+  a.loop = cand_flags(c, 0);
+  a.next = cand + 1 < p->nspec ? cand_flags(c, cand + 1) : nullptr;
   a.gate = gate_word(c);
-  a.cond = &c.at<Readback>(p->L.flags)->cond;
+  a.cond = cand_cond(c, cand);
   a.energy = c.at<double>(p->L.sys[1]) + p->energy_off;
   a.ctl = c.at<Control>(p->L.ctl);
   a.poses_dst = c.at<double>(p->L.poses[0]);
@@ -901,7 +923,7 @@ DecideArgs decide_args(Ctx& c) {
 
 // energy-only trial pass (energy_kernel): d_n by back-substitution at x_c (when
 // `backsub`) and the energy at x_n, partials in part_energy
-int launch_epass(Ctx& c, int cur, int nxt, bool backsub) {
+int launch_epass(Ctx& c, int cur, int nxt, bool backsub, int cand = 0) {
   dba_plan* p = c.p;
   if (p->NL == 0) return DBA_OK;
   EnergyArgs a;
@@ -912,7 +934,7 @@ int launch_epass(Ctx& c, int cur, int nxt, bool backsub) {
   a.kmax = std::max(p->kmax, 1);
   a.backsub = backsub ? 1 : 0;
   a.freeze = p->freeze_d;
-  a.status = c.at<int>(p->L.flags);
+  a.status = cand_flags(c, cand);
   a.csr_off = c.at<int>(p->L.csr_off);
   a.slot_flow = c.at<int>(p->L.slot_flow);
   a.frame_of = c.at<int>(p->L.frame_of);
@@ -951,11 +973,11 @@ int launch_epass(Ctx& c, int cur, int nxt, bool backsub) {
   return DBA_OK;
 }
 
-int launch_decide(Ctx& c);
+int launch_decide(Ctx& c, int cand);
 
 // finalize the energy of `slot` [-> all-reduce of the energy and the bad-edge flag];
 // with `decide` the LM decision follows (fused into finalize on a single rank)
-int launch_energy(Ctx& c, int slot, bool decide, int* status, bool from_epass = false) {
+int launch_energy(Ctx& c, int slot, bool decide, int* status, bool from_epass = false, int cand = 0) {
   dba_plan* p = c.p;
   FinalArgs f;
   f.status = status;
@@ -971,7 +993,7 @@ int launch_energy(Ctx& c, int slot, bool decide, int* status, bool from_epass = 
   f.energy_out = c.at<double>(p->L.sys[slot]) + p->energy_off;
   const bool multi = c.comm && p->nranks > 1;
   if (decide && !multi) {
-    if (int s = launch(c, finalize_decide_kernel, dim3(1), dim3(256), 0, false, f, decide_args(c))) return s;
+    if (int s = launch(c, finalize_decide_kernel, dim3(1), dim3(256), 0, false, f, decide_args(c, cand))) return s;
     mark(c, "fin+decide");
     return DBA_OK;
   }
@@ -981,10 +1003,10 @@ int launch_energy(Ctx& c, int slot, bool decide, int* status, bool from_epass = 
     if (!nccl().ok) return DBA_ENCCL;
     double* e = c.at<double>(p->L.sys[slot]) + p->energy_off;
     if (nccl().AllReduce(e, e, 1, ncclDouble, ncclSum, c.comm, c.st) != ncclSuccess) return DBA_ENCCL;
-    int* bad = c.at<int>(p->L.flags) + 1;
+    int* bad = status + 1;
     if (nccl().AllReduce(bad, bad, 1, ncclInt32, ncclMin, c.comm, c.st) != ncclSuccess) return DBA_ENCCL;
   }
-  if (decide) return launch_decide(c);
+  if (decide) return launch_decide(c, cand);
   return DBA_OK;
 }
 
@@ -1045,7 +1067,8 @@ int launch_system(Ctx& c, int slot, bool decide = false, bool gated = false) {
   return launch_energy(c, slot, decide, status);
 }
 
-int launch_solve(Ctx& c, int slot) {
+// nspec damping candidates (CTA / CTA pair each): lambda, 10 lambda, ...
+int launch_solve(Ctx& c, int slot, int nspec = 1) {
   dba_plan* p = c.p;
   if (p->n_red == 0) return DBA_OK;
   SolveArgs a;
@@ -1066,6 +1089,15 @@ int launch_solve(Ctx& c, int slot) {
   a.delta = c.at<double>(p->L.delta);
   a.cond = &c.at<Readback>(p->L.flags)->cond;
   a.m_top = p->m_top;
+  a.nspec = nspec;
+  a.spec_Lband = p->spec_Lband;
+  a.spec_rLband = p->spec_rLband;
+  a.spec_mid = p->spec_mid;
+  a.spec_delta = p->spec_delta;
+  for (int k = 0; k < kMaxSpec; ++k) {
+    a.spec_status[k] = cand_flags(c, k);
+    a.spec_cond[k] = cand_cond(c, k);
+  }
   void (*kern)(const SolveArgs);
   if (p->two_sided)
     kern = (p->BW <= 5) ? solve2_kernel<1> : (p->BW <= 10) ? solve2_kernel<2> : solve2_kernel<5>;
@@ -1078,7 +1110,8 @@ int launch_solve(Ctx& c, int slot) {
     if (int s2 = ev_pair(c, ev)) return s2;
     DBA_CUDA(cudaEventRecord(pr.pool[ev.first], c.st));
   }
-  if (int s = launch(c, kern, dim3(p->two_sided ? 2 : 1), dim3(kSolveThreads), p->solve_smem, p->two_sided != 0, a))
+  if (int s = launch(c, kern, dim3(nspec * (p->two_sided ? 2 : 1)), dim3(kSolveThreads), p->solve_smem,
+                     p->two_sided != 0, a))
     return s;
   mark(c, "solve");
   pr.solve_launches++;
@@ -1089,7 +1122,9 @@ int launch_solve(Ctx& c, int slot) {
   return cuda_status(cudaGetLastError());
 }
 
-int launch_decide(Ctx& c) { return launch(c, decide_kernel, dim3(1), dim3(256), 0, false, decide_args(c)); }
+int launch_decide(Ctx& c, int cand) {
+  return launch(c, decide_kernel, dim3(1), dim3(256), 0, false, decide_args(c, cand));
+}
 
 int upload_control(Ctx& c, double lam, double Ec) {
   Control h{};
@@ -1105,6 +1140,7 @@ int reset_flags(Ctx& c) {
   Readback h{};
   h.status[0] = 0;
   h.status[1] = INT_MAX;
+  for (int k = 0; k < kMaxSpec - 1; ++k) h.spec[k][1] = INT_MAX;
   h.cond = 0.0;
   *c.p->rb = h;
   DBA_CUDA(cudaMemcpyAsync(c.at<Readback>(c.p->L.flags), c.p->rb, sizeof(Readback),
@@ -1195,14 +1231,18 @@ int dba_solve(dba_plan* p, const dba_options* o, const dba_buffers* b, dba_repor
   for (int seen = 0; o->iters > 0;) {
     const int batch = std::max(1, o->iters - seen);
     for (int t = 0; t < batch; ++t) {
-      // trial: solve, step, energy-only pass (back-substitution + residuals at x_n),
-      // decision; only an accepted trial that continues the loop is linearised
-      // (the same pass with the system, gated on the decision) -- rejected trials
-      // cost no Jacobians or Schur fill-in
-      if ((s = launch_solve(c, 0))) return rep->status = s;
-      if ((s = launch_prep(c, 0, 1, false))) return rep->status = s;
-      if ((s = launch_epass(c, 0, 1, true))) return rep->status = s;
-      if ((s = launch_energy(c, 1, true, c.at<int>(p->L.flags), true))) return rep->status = s;
+      // round: the reduced system is factored for nspec damping values at once
+      // (lambda, 10 lambda, ... -- the trials successive rejections would run); then,
+      // per candidate in order, step + energy-only pass (back-substitution and
+      // residuals at x_n) + decision, a candidate running only after the previous one
+      // was rejected; only an accepted trial that continues the loop is linearised
+      // (the full pass, gated on the decision)
+      if ((s = launch_solve(c, 0, p->nspec))) return rep->status = s;
+      for (int k = 0; k < p->nspec; ++k) {
+        if ((s = launch_prep(c, 0, 1, false, k))) return rep->status = s;
+        if ((s = launch_epass(c, 0, 1, true, k))) return rep->status = s;
+        if ((s = launch_energy(c, 1, true, cand_flags(c, k), true, k))) return rep->status = s;
+      }
       // accepted and continuing: linearise at the trial state straight into slot 0
       // (disparities d_n of slot 1 -> slot 0, system and gauge state of slot 0)
       if ((s = launch_pass(c, 1, 0, false, true, true))) return rep->status = s;

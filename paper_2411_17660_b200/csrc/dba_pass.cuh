@@ -170,7 +170,9 @@ __device__ __forceinline__ PixTerms pix_terms(const float R[9], const float t[3]
   const float Y = fmaf(R[3], qx, fmaf(R[4], qy, R[5])) + t[1] * d;
   const float Z = fmaf(R[6], qx, fmaf(R[7], qy, R[8])) + t[2] * d;
   bool ok = in && Z > 1e-4f * d;
-  o.iz = ok ? 1.f / Z : 0.f;
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(Z));  // <= 1 ulp; Z > 0 here
+  o.iz = ok ? r : 0.f;
   o.xt = X * o.iz;
   o.yt = Y * o.iz;
   const float pu = fmaf(fx, o.xt, cx), pv = fmaf(fy, o.yt, cy);

@@ -51,6 +51,7 @@ constexpr int kWB = 38;
 #define DBA_KTR 3
 #endif
 constexpr int kTR = DBA_KTR;  // rows of a trailing-update output block per thread
+constexpr int kMaxSpec = 3;   // damping candidates solved per round (lambda, 10 lambda, 100 lambda)
 
 struct SolveArgs {
   int nb, BW, calib;
@@ -67,7 +68,28 @@ struct SolveArgs {
   double* delta;        // 6 nb + 4 calib
   double* cond;         // theta pivot ratio
   int m_top;            // two-sided: pivots of the top chain (0: one-sided)
+  // speculative damping: candidate k (one CTA / CTA pair each) factors S + 10^k lambda I
+  // into its own factor rows, exchange scratch, step, flags word and condition slot,
+  // so the trials a rejection would run next are already solved
+  int nspec;
+  long long spec_Lband, spec_rLband, spec_mid, spec_delta;  // per-candidate strides (doubles)
+  int* spec_status[kMaxSpec];
+  double* spec_cond[kMaxSpec];
 };
+
+// the arguments of candidate k (k = 0: the controller's lambda)
+__device__ __forceinline__ SolveArgs spec_view(const SolveArgs& A, int k, double& lam) {
+  SolveArgs B = A;
+  B.Lband += k * A.spec_Lband;
+  B.rLband += k * A.spec_rLband;
+  B.mid += k * A.spec_mid;
+  B.delta += k * A.spec_delta;
+  B.status = A.spec_status[k];
+  B.cond = A.spec_cond[k];
+  lam = *A.lambda;
+  for (int i = 0; i < k; ++i) lam *= 10.0;  // the controller's own sequence after k rejections
+  return B;
+}
 
 // doubles of the two-sided exchange scratch
 __host__ __device__ inline long long solve_mid_len(int BW) {
@@ -689,10 +711,11 @@ __device__ inline ChainSm chain_sm(unsigned char* smem, const SolveSmem& L, int*
 
 // one-sided solve (small systems)
 template <int NS>
-__global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const SolveArgs A) {
+__global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const SolveArgs A0) {
   pdl_enter();
-  if (A.status[3] != 0) return;  // GN loop finished
-  const double lam = *A.lambda;
+  if (A0.status[3] != 0) return;  // GN loop finished
+  double lam;
+  const SolveArgs A = spec_view(A0, blockIdx.x, lam);
   extern __shared__ __align__(16) unsigned char smem[];
   const SolveSmem L = solve_smem_layout(A.nb, A.BW, A.calib);
   __shared__ int fail;
@@ -722,17 +745,18 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const SolveArgs
 
 // two-sided solve: 2 cooperative CTAs (see the header comment)
 template <int NS>
-__global__ void __launch_bounds__(kSolveThreads, 1) solve2_kernel(const SolveArgs A) {
+__global__ void __launch_bounds__(kSolveThreads, 1) solve2_kernel(const SolveArgs A0) {
   pdl_enter();
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
-  if (A.status[3] != 0) return;  // GN loop finished (uniform over both CTAs)
-  const double lam = *A.lambda;
+  if (A0.status[3] != 0) return;  // GN loop finished (uniform over the grid)
+  double lam;
+  const SolveArgs A = spec_view(A0, blockIdx.x >> 1, lam);  // CTA pair per candidate
   extern __shared__ __align__(16) unsigned char smem[];
   const SolveSmem L = solve_smem_layout(A.nb, A.BW, A.calib);
   __shared__ int fail;
   __shared__ double xts[4];
-  const int tid = threadIdx.x, cta = blockIdx.x;
+  const int tid = threadIdx.x, cta = blockIdx.x & 1;
   const int nb = A.nb, BW = A.BW, W1 = BW + 1, NR = W1 * 36;
   const int calib = A.calib;
   const int m = A.m_top, mb = nb - m - BW;  // pivots of the top / bottom chain

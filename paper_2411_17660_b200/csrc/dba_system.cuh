@@ -477,7 +477,9 @@ struct Control {
 struct DecideArgs {
   int iters, calib;
   double lam_min, lam_max, cond_max;
-  int* status;          // flags word
+  int* status;          // flags word of this damping candidate ([0] failed, [1] bad edge, [3] skip)
+  int* loop;            // the loop's flags word ([3] finished; == status for candidate 0)
+  int* next;            // flags word of the next candidate, or null
   int* gate;            // flags word of the kernels that linearise an accepted trial
   double* cond;         // theta pivot ratio of the last solve
   const double* energy; // energy of the trial state (slot 1)
@@ -492,11 +494,31 @@ struct DecideArgs {
   const double* intr_src;
 };
 
-__device__ void gn_decide(const DecideArgs& A) {
+// One LM decision on the trial of one damping candidate.  Candidates are decided in
+// order (lambda, 10 lambda, ...) exactly as the sequential schedule would run them:
+// candidate k is only evaluated when every earlier one was rejected or failed, so
+// the decisions, lambda sequence, trial count and trace are those of one-at-a-time
+// trials.  Returns false when the candidate was not needed (no state change beyond
+// propagating the skip).
+__device__ bool gn_decide(const DecideArgs& A) {
   Control* c = A.ctl;
   int* st = A.status;
+  int* lp = A.loop;
+  const bool first = st == lp;
+  if (lp[3] != 0 || (!first && st[3] != 0)) {  // finished, or an earlier candidate decided
+    if (!first) {
+      st[0] = 0;
+      st[1] = INT_MAX;
+      st[2] = 0;
+    }
+    if (A.next) {
+      A.next[3] = 1;
+      A.next[0] = 0;
+      A.next[2] = 0;
+    }
+    return false;
+  }
   c->accept = 0;
-  if (st[3] != 0) return;
   int done = 0;
   if (st[0] != 0) {  // factorisation failed: more damping, same iterate
     c->lam *= 10.0;
@@ -544,18 +566,27 @@ __device__ void gn_decide(const DecideArgs& A) {
   st[0] = 0;
   st[1] = INT_MAX;
   st[2] = 0;
-  st[3] = done;
+  if (first) st[3] = done;
+  else st[3] = 0;
+  lp[3] = done;
+  if (A.next) {  // the next candidate runs only after a rejection / failure
+    const int skip = c->accept || done;
+    A.next[3] = skip;
+    A.next[1] = INT_MAX;
+    if (skip) {
+      A.next[0] = 0;
+      A.next[2] = 0;
+    }
+  }
   *A.cond = 0.0;
+  return true;
 }
 
 // the LM decision (thread 0) and, on acceptance, the pose/intrinsics copy by the
 // whole block
 __device__ void decide_block(const DecideArgs& A) {
   __shared__ int acc;
-  if (threadIdx.x == 0) {
-    gn_decide(A);
-    acc = A.ctl->accept;
-  }
+  if (threadIdx.x == 0) acc = gn_decide(A) && A.ctl->accept;
   __syncthreads();
   if (acc) {
     for (int x = threadIdx.x; x < A.pose_words; x += blockDim.x) A.poses_dst[x] = A.poses_src[x];
