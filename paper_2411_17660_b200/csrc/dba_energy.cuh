@@ -18,10 +18,14 @@
 
 namespace dba {
 
-constexpr int kEnergyThreads = 256;
+constexpr int kEnergyTile = 256;                   // pixels per CTA (one tile of one frame)
+// pixels per thread: 2 and 4 (independent chains, fewer CTA-setup instructions) measured
+// no faster than 1 (65.5 / 80.6 us vs 65.6 us on C3: fewer resident warps)
+constexpr int kEnergyPx = 1;
+constexpr int kEnergyThreads = kEnergyTile / kEnergyPx;
 
 struct EnergyArgs {
-  int H, W, P, tiles;  // tiles = ceil(P / 256) per frame
+  int H, W, P, tiles;  // tiles = ceil(P / kEnergyTile) per frame
   int kmax;
   int backsub, freeze;
   const int* status;
@@ -46,11 +50,11 @@ struct EnergyArgs {
 
 // flow records of the thread's pixel are staged in shared memory (cp.async, one
 // burst per CTA) when the frame's out-degree allows (else both walks read through L1)
-constexpr int kEnergyStageMax = 16;
+constexpr int kEnergyStageMax = 16;  // without staging: 72 us vs 66 us on C3
 
 __host__ __device__ inline size_t energy_smem_bytes(int kmax) {
   const size_t k = (size_t)(kmax > 0 ? kmax : 1);
-  const size_t stage = kmax <= kEnergyStageMax ? sizeof(float4) * kEnergyThreads * k : 0;
+  const size_t stage = kmax <= kEnergyStageMax ? sizeof(float4) * kEnergyTile * k : 0;
   return stage + (sizeof(EdgeLin) + sizeof(EdgeBack) + sizeof(float4*)) * k;
 }
 
@@ -90,7 +94,7 @@ __global__ void __launch_bounds__(kEnergyThreads) energy_kernel(const EnergyArgs
   const int f = A.frame_of[fl];
   const bool stage = A.kmax <= kEnergyStageMax;
   float4* fs = reinterpret_cast<float4*>(smem);  // [k][256] when staged
-  EdgeLin* sl = reinterpret_cast<EdgeLin*>(smem + (stage ? sizeof(float4) * kEnergyThreads * A.kmax : 0));
+  EdgeLin* sl = reinterpret_cast<EdgeLin*>(smem + (stage ? sizeof(float4) * kEnergyTile * A.kmax : 0));
   EdgeBack* sb = reinterpret_cast<EdgeBack*>(sl + k);
   const float4** fp0 = reinterpret_cast<const float4**>(sb + k);
   const int tid = threadIdx.x;
@@ -115,83 +119,123 @@ __global__ void __launch_bounds__(kEnergyThreads) energy_kernel(const EnergyArgs
   }
   __syncthreads();
 
-  const int p = tile * kEnergyThreads + tid;
-  const bool in = p < P;
-  const int pc = in ? p : 0;  // clamped: out-of-range lanes read pixel 0 and contribute nothing
-  // the thread's k flow records -> shared memory in one burst (each thread reads back
-  // only its own, so no barrier); without staging both walks read through L1
+  // the thread's pixels p_j = tile*256 + j*kEnergyThreads + tid, each with its k flow
+  // records staged in shared memory in one burst (each thread reads back only its own,
+  // so no barrier); without staging both walks read through L1
+  bool in[kEnergyPx];
+  int pc[kEnergyPx];
+#pragma unroll
+  for (int j = 0; j < kEnergyPx; ++j) {
+    const int p = tile * kEnergyTile + j * kEnergyThreads + tid;
+    in[j] = p < P;
+    pc[j] = in[j] ? p : 0;  // clamped: out-of-range pixels read pixel 0 and contribute nothing
+  }
   if (stage) {
-    for (int a = 0; a < k; ++a) {
-      const unsigned dst = (unsigned)__cvta_generic_to_shared(fs + a * kEnergyThreads + tid);
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(fp0[a] + pc));
-    }
+    for (int a = 0; a < k; ++a)
+#pragma unroll
+      for (int j = 0; j < kEnergyPx; ++j) {
+        const unsigned dst =
+            (unsigned)__cvta_generic_to_shared(fs + a * kEnergyTile + j * kEnergyThreads + tid);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(fp0[a] + pc[j]));
+      }
     asm volatile("cp.async.commit_group;");
   }
-  auto record = [&](int a) -> float4 { return stage ? fs[a * kEnergyThreads + tid] : __ldg(fp0[a] + pc); };
+  auto record = [&](int a, int j) -> float4 {
+    return stage ? fs[a * kEnergyTile + j * kEnergyThreads + tid] : __ldg(fp0[a] + pc[j]);
+  };
   const float Wf = (float)A.W, Hf = (float)A.H;
   const float fxn = (float)A.intr_n[0], fyn = (float)A.intr_n[1];
   const float cxn = (float)A.intr_n[2], cyn = (float)A.intr_n[3];
-  const float pu = (float)(pc % A.W), pv = (float)(pc / A.W);
-  const size_t fpx = (size_t)f * P + pc;
-  const float dc = A.d_cur[fpx];
-  float dn = dc;
-  float ap = 0.f;
-  if (A.prior != nullptr) ap = A.alpha * (A.pweight ? A.pweight[f] : 1.f) * (float)A.pmask[fpx];
+  float pu[kEnergyPx], pv[kEnergyPx], dc[kEnergyPx], dn[kEnergyPx], ap[kEnergyPx];
+#pragma unroll
+  for (int j = 0; j < kEnergyPx; ++j) {
+    pu[j] = (float)(pc[j] % A.W);
+    pv[j] = (float)(pc[j] / A.W);
+    const size_t fpx = (size_t)f * P + pc[j];
+    dc[j] = A.d_cur[fpx];
+    dn[j] = dc[j];
+    ap[j] = A.prior != nullptr ? A.alpha * (A.pweight ? A.pweight[f] : 1.f) * (float)A.pmask[fpx] : 0.f;
+  }
   if (stage) asm volatile("cp.async.wait_all;" ::: "memory");
   if (phaseA) {
     const float fxc = (float)A.intr_c[0], fyc = (float)A.intr_c[1];
     const float cxc = (float)A.intr_c[2], cyc = (float)A.intr_c[3];
     const float dth[4] = {(float)(A.intr_n[0] - A.intr_c[0]), (float)(A.intr_n[1] - A.intr_c[1]),
                           (float)(A.intr_n[2] - A.intr_c[2]), (float)(A.intr_n[3] - A.intr_c[3])};
-    const float qx = (pu - cxc) / fxc, qy = (pv - cyc) / fyc;
-    float Cp = 0.f, gdp = 0.f, accp = 0.f;
+    float qx[kEnergyPx], qy[kEnergyPx], Cp[kEnergyPx], gdp[kEnergyPx], accp[kEnergyPx];
+#pragma unroll
+    for (int j = 0; j < kEnergyPx; ++j) {
+      qx[j] = (pu[j] - cxc) / fxc;
+      qy[j] = (pv[j] - cyc) / fyc;
+      Cp[j] = gdp[j] = accp[j] = 0.f;
+    }
     for (int a = 0; a < k; ++a) {
-      const float4 fw = record(a);
       const EdgeBack& e = sb[a];
-      const PixTerms T = pix_terms_e(reinterpret_cast<const EdgeLin&>(e), qx, qy, dc, fxc, fyc, cxc, cyc, Wf, Hf, fw);
-      const float fxi = fxc * T.iz, fyi = fyc * T.iz;
-      const float Jdu = fxi * (e.t[0] - T.xt * e.t[2]);
-      const float Jdv = fyi * (e.t[1] - T.yt * e.t[2]);
-      const float* dl = e.dlt;
-      float ju = fxi * dc * (dl[0] - T.xt * dl[2]) +
-                 fxc * (-T.xt * T.yt * dl[3] + (1.f + T.xt * T.xt) * dl[4] - T.yt * dl[5]);
-      float jv = fyi * dc * (dl[1] - T.yt * dl[2]) +
-                 fyc * (-(1.f + T.yt * T.yt) * dl[3] + T.xt * T.yt * dl[4] + T.xt * dl[5]);
-      if (CALIB) {
-        const float cu0 = T.iz * (e.R[0] - T.xt * e.R[6]), cu1 = T.iz * (e.R[1] - T.xt * e.R[7]);
-        const float cv0 = T.iz * (e.R[3] - T.yt * e.R[6]), cv1 = T.iz * (e.R[4] - T.yt * e.R[7]);
-        ju += (T.xt - cu0 * qx) * dth[0] + (-cu1 * qy * fxc / fyc) * dth[1] + (1.f - cu0) * dth[2] +
-              (-cu1 * fxc / fyc) * dth[3];
-        jv += (-cv0 * qx * fyc / fxc) * dth[0] + (T.yt - cv1 * qy) * dth[1] + (-cv0 * fyc / fxc) * dth[2] +
-              (1.f - cv1) * dth[3];
+#pragma unroll
+      for (int j = 0; j < kEnergyPx; ++j) {
+        const float4 fw = record(a, j);
+        const PixTerms T =
+            pix_terms_e(reinterpret_cast<const EdgeLin&>(e), qx[j], qy[j], dc[j], fxc, fyc, cxc, cyc, Wf, Hf, fw);
+        const float fxi = fxc * T.iz, fyi = fyc * T.iz;
+        const float Jdu = fxi * (e.t[0] - T.xt * e.t[2]);
+        const float Jdv = fyi * (e.t[1] - T.yt * e.t[2]);
+        const float* dl = e.dlt;
+        float ju = fxi * dc[j] * (dl[0] - T.xt * dl[2]) +
+                   fxc * (-T.xt * T.yt * dl[3] + (1.f + T.xt * T.xt) * dl[4] - T.yt * dl[5]);
+        float jv = fyi * dc[j] * (dl[1] - T.yt * dl[2]) +
+                   fyc * (-(1.f + T.yt * T.yt) * dl[3] + T.xt * T.yt * dl[4] + T.xt * dl[5]);
+        if (CALIB) {
+          const float cu0 = T.iz * (e.R[0] - T.xt * e.R[6]), cu1 = T.iz * (e.R[1] - T.xt * e.R[7]);
+          const float cv0 = T.iz * (e.R[3] - T.yt * e.R[6]), cv1 = T.iz * (e.R[4] - T.yt * e.R[7]);
+          ju += (T.xt - cu0 * qx[j]) * dth[0] + (-cu1 * qy[j] * fxc / fyc) * dth[1] + (1.f - cu0) * dth[2] +
+                (-cu1 * fxc / fyc) * dth[3];
+          jv += (-cv0 * qx[j] * fyc / fxc) * dth[0] + (T.yt - cv1 * qy[j]) * dth[1] +
+                (-cv0 * fyc / fxc) * dth[2] + (1.f - cv1) * dth[3];
+        }
+        const float au = T.wu * Jdu, av = T.wv * Jdv;
+        Cp[j] += fmaf(au, Jdu, av * Jdv);
+        gdp[j] += fmaf(au, T.ru, av * T.rv);
+        accp[j] += fmaf(au, ju, av * jv);
       }
-      const float au = T.wu * Jdu, av = T.wv * Jdv;
-      Cp += fmaf(au, Jdu, av * Jdv);
-      gdp += fmaf(au, T.ru, av * T.rv);
-      accp += fmaf(au, ju, av * jv);
     }
-    float C = A.eta + Cp, gd = gdp;
-    if (A.prior != nullptr) {
-      C += ap;
-      gd += ap * (A.prior[fpx] - dc);
+#pragma unroll
+    for (int j = 0; j < kEnergyPx; ++j) {
+      float C = A.eta + Cp[j], gd = gdp[j];
+      if (A.prior != nullptr) {
+        C += ap[j];
+        gd += ap[j] * (A.prior[(size_t)f * P + pc[j]] - dc[j]);
+      }
+      float dd = (gd - accp[j]) / C;
+      if (gauge) dd -= (float)(kappa_s / (double)dc[j]);  // A5: r/C - kappa/d
+      dn[j] = fmaxf(dc[j] + dd, A.d_min);
     }
-    float dd = (gd - accp) / C;
-    if (gauge) dd -= (float)(kappa_s / (double)dc);  // A5: r/C - kappa/d
-    dn = fmaxf(dc + dd, A.d_min);
   }
-  if (in) A.d_new[fpx] = dn;
   // residual energy at (x_n, d_n)
-  const float qx = (pu - cxn) / fxn, qy = (pv - cyn) / fyn;
-  float en = 0.f;
-  for (int a = 0; a < k; ++a) {
-    const float4 fw = record(a);
-    const PixTerms T = pix_terms_e(sl[a], qx, qy, dn, fxn, fyn, cxn, cyn, Wf, Hf, fw);
-    en += T.wu * T.ru * T.ru + T.wv * T.rv * T.rv;
+  float qx[kEnergyPx], qy[kEnergyPx], en[kEnergyPx];
+#pragma unroll
+  for (int j = 0; j < kEnergyPx; ++j) {
+    if (in[j]) A.d_new[(size_t)f * P + pc[j]] = dn[j];
+    qx[j] = (pu[j] - cxn) / fxn;
+    qy[j] = (pv[j] - cyn) / fyn;
+    en[j] = 0.f;
   }
-  double ed = in ? (double)en : 0.0;
-  if (A.prior != nullptr && in) {
-    const float dd = A.prior[fpx] - dn;
-    ed += (double)(ap * dd * dd);
+  for (int a = 0; a < k; ++a) {
+    const EdgeLin& e = sl[a];
+#pragma unroll
+    for (int j = 0; j < kEnergyPx; ++j) {
+      const PixTerms T = pix_terms_e(e, qx[j], qy[j], dn[j], fxn, fyn, cxn, cyn, Wf, Hf, record(a, j));
+      en[j] += T.wu * T.ru * T.ru + T.wv * T.rv * T.rv;
+    }
+  }
+  double ed = 0.0;
+#pragma unroll
+  for (int j = 0; j < kEnergyPx; ++j) {
+    if (!in[j]) continue;
+    ed += (double)en[j];
+    if (A.prior != nullptr) {
+      const float dd = A.prior[(size_t)f * P + pc[j]] - dn[j];
+      ed += (double)(ap[j] * dd * dd);
+    }
   }
   // fixed-order block reduction
 #pragma unroll

@@ -570,7 +570,7 @@ int dba_plan_create(const dba_problem_desc* d, dba_plan** out) {
   L.part_M = take(sizeof(double) * n_pM);
   L.part_w = take(sizeof(double) * n_pw);
   L.part_frame = take(sizeof(double) * kFrameVals * (size_t)p->nseg);
-  L.part_energy = take(sizeof(double) * (size_t)std::max(p->NL, 1) * ((p->P + kEnergyThreads - 1) / kEnergyThreads));
+  L.part_energy = take(sizeof(double) * (size_t)std::max(p->NL, 1) * ((p->P + kEnergyTile - 1) / kEnergyTile));
   L.Fbuf = take(sizeof(double) * nF);
   // factor rows / exchange scratch per damping candidate
   p->spec_Lband = align_doubles(std::max<long long>(p->band_len, 1));
@@ -930,7 +930,7 @@ int launch_epass(Ctx& c, int cur, int nxt, bool backsub, int cand = 0) {
   a.H = p->H;
   a.W = p->W;
   a.P = p->P;
-  a.tiles = (p->P + kEnergyThreads - 1) / kEnergyThreads;
+  a.tiles = (p->P + kEnergyTile - 1) / kEnergyTile;
   a.kmax = std::max(p->kmax, 1);
   a.backsub = backsub ? 1 : 0;
   a.freeze = p->freeze_d;
@@ -982,7 +982,7 @@ int launch_energy(Ctx& c, int slot, bool decide, int* status, bool from_epass = 
   FinalArgs f;
   f.status = status;
   if (from_epass) {  // per-CTA partials of energy_kernel
-    f.n = p->NL * ((p->P + kEnergyThreads - 1) / kEnergyThreads);
+    f.n = p->NL * ((p->P + kEnergyTile - 1) / kEnergyTile);
     f.stride = 1;
     f.part_frame = c.at<double>(p->L.part_energy);
   } else {  // per-segment partials of pass_kernel
