@@ -96,6 +96,9 @@ typedef struct {
   double d_min;         /* disparity floor (1e-6) */
   double tangent_max;   /* per-pose tangent clamp (1) */
   double calib_cond_max;/* A9 degeneracy threshold */
+  int32_t damping_candidates; /* lambda values factored per round by dba_solve (lambda, 10 lambda,
+                                 ...; 0 = default 3, max 3).  A rejection then costs no new
+                                 factorisation; results are identical for every value. */
 } dba_options;
 
 typedef struct {

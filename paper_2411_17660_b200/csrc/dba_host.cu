@@ -95,7 +95,7 @@ struct dba_plan {
   size_t pass_smem = 0, solve_smem = 0;
   long long sys_len = 0;  // doubles in one packed reduced system
   long long spec_delta = 0, spec_Lband = 0, spec_rLband = 0, spec_mid = 0;  // per damping candidate
-  int nspec = kMaxSpec;  // damping candidates solved per round by dba_solve
+  int nspec = kMaxSpec;  // damping candidates solved per round by dba_solve (dba_options)
   long long band_len = 0, rband_off = 0, theta_off = 0, thth_off = 0, y_off = 0, energy_off = 0;
   int two_sided = 0, m_top = 0;  // two-CTA solve: pivots of the top chain
   std::vector<int> fixed_ridx;
@@ -756,6 +756,7 @@ int check_args(dba_plan* p, const dba_options* o, const dba_buffers* b) {
     // allowed only for dba_build_system (partial systems); dba_solve checks itself
   }
   if (!(o->eta > 0.0) || !(o->lambda0 > 0.0) || o->iters < 0) return DBA_EINVAL;
+  if (o->damping_candidates < 0 || o->damping_candidates > kMaxSpec) return DBA_EINVAL;
   return DBA_OK;
 }
 
@@ -1228,6 +1229,7 @@ int dba_solve(dba_plan* p, const dba_options* o, const dba_buffers* b, dba_repor
   ctl.lam = o->lambda0;
   ctl.Ec = Ec;
   ctl.bad_edge = -1;
+  p->nspec = o->damping_candidates > 0 ? o->damping_candidates : kMaxSpec;
   for (int seen = 0; o->iters > 0;) {
     const int batch = std::max(1, o->iters - seen);
     for (int t = 0; t < batch; ++t) {

@@ -32,7 +32,7 @@ from .errors import (CalibrationDegenerateError, CapacityError, ConfigError, Num
                      SolverFailure)
 
 DEFAULTS = dict(lambda0=1e-4, lambda_min=1e-8, lambda_max=1e6, eta=1e-4, alpha=1e-3,
-                d_min=1e-6, tangent_max=1.0, calib_cond_max=1e8)
+                d_min=1e-6, tangent_max=1.0, calib_cond_max=1e8, damping_candidates=0)
 
 
 # ----------------------------------------------------------------------------- SPEC types
@@ -212,7 +212,8 @@ class DBASolver:
         o = dict(DEFAULTS)
         o.update({k: v for k, v in kw.items() if v is not None})
         return _lib.Options(int(iters), o["lambda0"], o["lambda_min"], o["lambda_max"], o["eta"],
-                            o["alpha"], o["d_min"], o["tangent_max"], o["calib_cond_max"])
+                            o["alpha"], o["d_min"], o["tangent_max"], o["calib_cond_max"],
+                            int(o["damping_candidates"]))
 
     def _inputs(self, poses, disps, intr, flow, prior, prior_mask, prior_weight=None):
         dev = self.device

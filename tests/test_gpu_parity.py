@@ -229,3 +229,24 @@ def test_sharded_partial_systems_sum_to_full(torch_cuda, nranks):
     assert _rel(Ss, S) < 1e-10, _rel(Ss, S)
     assert _rel(ys, y) < 1e-10, _rel(ys, y)
     assert abs(es - e) <= 1e-10 * e
+
+
+@pytest.mark.parametrize("name,kf,calib", [("C1", None, False), ("C3", 64, False), ("C5", 60, True)])
+def test_damping_candidates_bitwise(torch_cuda, name, kf, calib):
+    """Speculative damping (lambda, 10 lambda, 100 lambda factored in one round) must
+    reproduce the one-trial-at-a-time schedule exactly: same decisions, trial count,
+    energy trace and bit-identical outputs.  iters=12 reaches the fp32 noise floor, where
+    trials are rejected."""
+    from paper_2411_17660_b200 import dba, scenes
+    wl = scenes.make_workload(name, height=24, width=32, keyframes=kf)
+    s = dba.DBASolver(wl.ii, wl.jj, len(wl.frames), 24, 32, wl.fixed, optimize_intrinsics=calib)
+    outs = []
+    for nc in (1, 2, 3):
+        Po, Do, Ko, rep = s.solve(wl.poses0, wl.disps0, wl.intr0, wl.flow, iters=12, damping_candidates=nc)
+        outs.append((Po.cpu().numpy(), Do.cpu().numpy(), Ko.cpu().numpy(), rep))
+    P1, D1, K1, r1 = outs[0]
+    for P, D, K, r in outs[1:]:
+        assert np.array_equal(P, P1) and np.array_equal(D, D1) and np.array_equal(K, K1)
+        assert (r.trials, r.iterations_run, r.converged) == (r1.trials, r1.iterations_run, r1.converged)
+        assert r.final_energy == r1.final_energy and r.lambda_final == r1.lambda_final
+        assert list(r.energy_trace) == list(r1.energy_trace)

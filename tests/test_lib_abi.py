@@ -97,8 +97,8 @@ def test_ctypes_struct_layout_matches_header():
 int main(void) {
   printf("%zu %zu %zu %zu %zu %zu\n", sizeof(dba_problem_desc), sizeof(dba_options),
          sizeof(dba_buffers), sizeof(dba_report), sizeof(dba_plan_info), sizeof(dba_stats));
-  printf("%zu %zu %zu\n", offsetof(dba_report, energy_trace), offsetof(dba_buffers, nccl_comm),
-         offsetof(dba_options, calib_cond_max));
+  printf("%zu %zu %zu %zu\n", offsetof(dba_report, energy_trace), offsetof(dba_buffers, nccl_comm),
+         offsetof(dba_options, calib_cond_max), offsetof(dba_options, damping_candidates));
   return 0;
 }'''
     with tempfile.TemporaryDirectory() as d:
@@ -113,3 +113,4 @@ int main(void) {
     assert sizes[6] == _lib.Report.energy_trace.offset
     assert sizes[7] == _lib.Buffers.nccl_comm.offset
     assert sizes[8] == _lib.Options.calib_cond_max.offset
+    assert sizes[9] == _lib.Options.damping_candidates.offset
