@@ -16,6 +16,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <new>
 #include <set>
 #include <utility>
@@ -64,6 +65,8 @@ constexpr size_t kAlign = 256;
 inline size_t align_up(size_t x) { return (x + kAlign - 1) & ~(kAlign - 1); }
 inline long long align_doubles(long long n) { return (long long)(align_up(sizeof(double) * (size_t)n) / sizeof(double)); }
 
+static_assert(kMaxSpec == kMaxSpecD, "damping candidate count");
+
 struct Readback {
   int status[4];  // flags word, see trial_skipped (dba_common.cuh)
   int gate[4];    // flags word of the accepted-trial linearisation (gn_decide)
@@ -96,6 +99,18 @@ struct dba_plan {
   long long sys_len = 0;  // doubles in one packed reduced system
   long long spec_delta = 0, spec_Lband = 0, spec_rLband = 0, spec_mid = 0;  // per damping candidate
   int nspec = kMaxSpec;  // damping candidates solved per round by dba_solve (dba_options)
+  // dba_solve's LM loop as one CUDA graph: WHILE(not finished) { solve; candidate 0;
+  // IF(candidate 1 needed) {...}; IF(candidate 2 needed) {...}; IF(accepted) {linearise} },
+  // conditions set by the decision kernels.  Rebuilt when its key (buffers, options)
+  // changes.
+  struct LoopGraph {
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    cudaStream_t cap = nullptr;
+    std::vector<unsigned char> key;
+    cudaGraphConditionalHandle h_loop = 0, h_lin = 0, h_cand[kMaxSpec] = {};
+    int nodes_round = 0, nodes_cand = 0, nodes_lin = 0;  // kernels per segment (launch accounting)
+  } lg;
   long long band_len = 0, rband_off = 0, theta_off = 0, thth_off = 0, y_off = 0, energy_off = 0;
   int two_sided = 0, m_top = 0;  // two-CTA solve: pivots of the top chain
   std::vector<int> fixed_ridx;
@@ -614,6 +629,9 @@ void dba_plan_destroy(dba_plan* p) {
   if (p->meta_pinned) cudaFreeHost(p->meta_pinned);
   if (p->rb) cudaFreeHost(p->rb);
   if (p->ctl_h) cudaFreeHost(p->ctl_h);
+  if (p->lg.exec) cudaGraphExecDestroy(p->lg.exec);
+  if (p->lg.graph) cudaGraphDestroy(p->lg.graph);
+  if (p->lg.cap) cudaStreamDestroy(p->lg.cap);
   delete p;
 }
 
@@ -652,6 +670,7 @@ struct Ctx {
   cudaStream_t st;
   unsigned char* ws;
   ncclComm_t comm;
+  bool graph = false;  // capturing the loop graph: decisions steer its conditional nodes
   template <typename T>
   T* at(size_t off) const {
     return reinterpret_cast<T*>(ws + off);
@@ -919,6 +938,12 @@ DecideArgs decide_args(Ctx& c, int cand = 0) {
   a.pose_words = 7 * p->N;
   a.intr_dst = c.at<double>(p->L.intr[0]);
   a.intr_src = c.at<double>(p->L.intr[1]);
+  a.graph = c.graph ? 1 : 0;
+  a.cand = cand;
+  a.nspec = p->nspec;
+  for (int k = 0; k < kMaxSpec; ++k) a.h_cand[k] = p->lg.h_cand[k];
+  a.h_lin = p->lg.h_lin;
+  a.h_loop = p->lg.h_loop;
   return a;
 }
 
@@ -1184,6 +1209,141 @@ int initial_pass(Ctx& c) {
   return launch_energy(c, 0, false, c.at<int>(p->L.flags), true);
 }
 
+// ---------------------------------------------------------------- LM loop graph
+// Segments are captured from the same launch helpers as the stream path into the
+// bodies of conditional nodes (WHILE over rounds, IF per later candidate, IF for the
+// linearisation), so both paths run identical kernels with identical arguments.
+int capture_into(Ctx& cc, cudaGraph_t g, const std::function<int(Ctx&)>& seg, std::vector<cudaGraphNode_t>* tail,
+                 int* kernels) {
+  cudaStream_t s = cc.st;
+  DBA_CUDA(cudaStreamBeginCaptureToGraph(s, g, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+  const long long l0 = cc.p->prof.launches;
+  const int rc = seg(cc);
+  *kernels = (int)(cc.p->prof.launches - l0);
+  cc.p->prof.launches = l0;
+  if (tail) {
+    cudaStreamCaptureStatus st;
+    const cudaGraphNode_t* deps = nullptr;
+    size_t nd = 0;
+    if (cudaStreamGetCaptureInfo(s, &st, nullptr, nullptr, &deps, &nd) == cudaSuccess) tail->assign(deps, deps + nd);
+  }
+  cudaGraph_t out = nullptr;
+  const cudaError_t e = cudaStreamEndCapture(s, &out);
+  if (rc) return rc;
+  return cuda_status(e);
+}
+
+int add_conditional(cudaGraph_t g, const std::vector<cudaGraphNode_t>& deps, cudaGraphConditionalHandle h,
+                    cudaGraphConditionalNodeType type, cudaGraphNode_t* node, cudaGraph_t* body) {
+  cudaGraphNodeParams q = {};
+  q.type = cudaGraphNodeTypeConditional;
+  q.conditional.handle = h;
+  q.conditional.type = type;
+  q.conditional.size = 1;
+  DBA_CUDA(cudaGraphAddNode(node, g, deps.data(), deps.size(), &q));
+  *body = q.conditional.phGraph_out[0];
+  return DBA_OK;
+}
+
+std::vector<unsigned char> loop_key(const Ctx& c) {
+  std::vector<unsigned char> k;
+  auto put_bytes = [&](const void* x, size_t n) {
+    const unsigned char* b = reinterpret_cast<const unsigned char*>(x);
+    k.insert(k.end(), b, b + n);
+  };
+  const void* ptrs[6] = {c.b->workspace, c.b->flow, c.b->prior, c.b->prior_mask, c.b->prior_weight, nullptr};
+  put_bytes(ptrs, sizeof(ptrs));
+  put_bytes(c.o, sizeof(dba_options));
+  put_bytes(&c.p->nspec, sizeof(int));
+  return k;
+}
+
+int build_loop_graph(Ctx& c) {
+  dba_plan* p = c.p;
+  auto& lg = p->lg;
+  if (lg.exec) cudaGraphExecDestroy(lg.exec);
+  if (lg.graph) cudaGraphDestroy(lg.graph);
+  lg.exec = nullptr;
+  lg.graph = nullptr;
+  lg.key.clear();
+  if (!lg.cap) DBA_CUDA(cudaStreamCreateWithFlags(&lg.cap, cudaStreamNonBlocking));
+  DBA_CUDA(cudaGraphCreate(&lg.graph, 0));
+  DBA_CUDA(cudaGraphConditionalHandleCreate(&lg.h_loop, lg.graph, 1, cudaGraphCondAssignDefault));
+  cudaGraphNode_t wnode;
+  cudaGraph_t body;
+  if (int s = add_conditional(lg.graph, {}, lg.h_loop, cudaGraphCondTypeWhile, &wnode, &body)) return s;
+  for (int k = 1; k < p->nspec; ++k) DBA_CUDA(cudaGraphConditionalHandleCreate(&lg.h_cand[k], body, 0, 0));
+  DBA_CUDA(cudaGraphConditionalHandleCreate(&lg.h_lin, body, 0, 0));
+  Ctx cc = c;
+  cc.st = lg.cap;
+  cc.graph = true;
+  std::vector<cudaGraphNode_t> tail;
+  auto cand_seg = [](int k) {
+    return [k](Ctx& x) -> int {
+      if (int s = launch_prep(x, 0, 1, false, k)) return s;
+      if (int s = launch_epass(x, 0, 1, true, k)) return s;
+      return launch_energy(x, 1, true, cand_flags(x, k), true, k);
+    };
+  };
+  int n0 = 0, nk = 0, nl = 0;
+  if (int s = capture_into(cc, body,
+                           [&](Ctx& x) -> int {
+                             if (int s2 = launch_solve(x, 0, x.p->nspec)) return s2;
+                             return cand_seg(0)(x);
+                           },
+                           &tail, &n0))
+    return s;
+  for (int k = 1; k < p->nspec; ++k) {
+    cudaGraphNode_t node;
+    cudaGraph_t kb;
+    if (int s = add_conditional(body, tail, lg.h_cand[k], cudaGraphCondTypeIf, &node, &kb)) return s;
+    if (int s = capture_into(cc, kb, cand_seg(k), nullptr, &nk)) return s;
+    tail.assign(1, node);
+  }
+  {
+    cudaGraphNode_t node;
+    cudaGraph_t lb;
+    if (int s = add_conditional(body, tail, lg.h_lin, cudaGraphCondTypeIf, &node, &lb)) return s;
+    if (int s = capture_into(cc, lb,
+                             [](Ctx& x) -> int {
+                               if (int s2 = launch_pass(x, 1, 0, false, true, true)) return s2;
+                               return launch_system(x, 0, false, true);
+                             },
+                             nullptr, &nl))
+      return s;
+  }
+  DBA_CUDA(cudaGraphInstantiate(&lg.exec, lg.graph, 0));
+  lg.nodes_round = n0;
+  lg.nodes_cand = nk;
+  lg.nodes_lin = nl;
+  lg.key = loop_key(c);
+  return DBA_OK;
+}
+
+// the whole LM loop as one graph launch (single rank, no profiling), opt-in with
+// DBA_GRAPH=1: measured equal to the PDL stream path on C3 (6.62 vs 6.63 ms per call) --
+// skipped launches already cost ~nothing with programmatic serialisation -- while a
+// caller that passes new buffers each call pays a re-instantiation (end-to-end 7.06e9
+// vs 7.37e9 edge-px/s)
+bool use_loop_graph(const Ctx& c) {
+  const char* e = std::getenv("DBA_GRAPH");
+  const bool on = e != nullptr && e[0] == '1';
+  return on && !c.p->prof.on && !c.p->prof.timeline && !(c.comm && c.p->nranks > 1) && c.p->n_red > 0 &&
+         c.p->NL > 0;
+}
+
+int run_loop_graph(Ctx& c) {
+  dba_plan* p = c.p;
+  if (!p->lg.exec || p->lg.key != loop_key(c)) {
+    if (int s = build_loop_graph(c)) {
+      cudaGetLastError();
+      return s;
+    }
+  }
+  DBA_CUDA(cudaGraphLaunch(p->lg.exec, c.st));
+  return DBA_OK;
+}
+
 int gauge_sum(Ctx& c, const float* d, double* out) {
   dba_plan* p = c.p;
   const int g = p->gauge_frame;
@@ -1230,7 +1390,20 @@ int dba_solve(dba_plan* p, const dba_options* o, const dba_buffers* b, dba_repor
   ctl.Ec = Ec;
   ctl.bad_edge = -1;
   p->nspec = o->damping_candidates > 0 ? o->damping_candidates : kMaxSpec;
-  for (int seen = 0; o->iters > 0;) {
+  // device-driven loop: one graph launch runs every round (conditional nodes skip the
+  // candidates and linearisations the decisions rule out); otherwise batches of rounds
+  // are enqueued on the stream until the controller reports done
+  bool graphed = false;
+  if (o->iters > 0 && use_loop_graph(c) && run_loop_graph(c) == DBA_OK) {
+    graphed = true;
+    DBA_CUDA(cudaMemcpyAsync(p->ctl_h, c.at<Control>(p->L.ctl), sizeof(Control), cudaMemcpyDeviceToHost, c.st));
+    DBA_CUDA(cudaStreamSynchronize(c.st));
+    ctl = *p->ctl_h;
+    const auto& lg = p->lg;
+    p->prof.launches += (long long)ctl.rounds * lg.nodes_round + (long long)(ctl.cands - ctl.rounds) * lg.nodes_cand +
+                        (long long)ctl.lins * lg.nodes_lin;
+  }
+  for (int seen = 0; !graphed && o->iters > 0;) {
     const int batch = std::max(1, o->iters - seen);
     for (int t = 0; t < batch; ++t) {
       // round: the reduced system is factored for nspec damping values at once

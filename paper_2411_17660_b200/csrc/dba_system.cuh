@@ -467,10 +467,12 @@ namespace dba {
 // linearisation of an accepted trial writes slot 0's disparities, system and gauge
 // state.
 constexpr int kTraceMax = 64;  // == DBA_TRACE_MAX
+constexpr int kMaxSpecD = 3;   // == kMaxSpec (dba_solve.cuh)
 
 struct Control {
   double lam, Ec, cond;
   int it, trials, result, converged, bad_edge, accept, done, pad;
+  int rounds, cands, lins, pad2;  // executed rounds / candidate decisions / linearisations
   double trace[kTraceMax];
 };
 
@@ -492,6 +494,10 @@ struct DecideArgs {
   int pose_words;
   double* intr_dst;
   const double* intr_src;
+  // graph mode (dba_solve's device-driven loop): the decision also steers the
+  // conditional nodes -- the next candidate's IF, the linearisation IF, the WHILE
+  int graph, cand, nspec;
+  unsigned long long h_cand[kMaxSpecD], h_lin, h_loop;
 };
 
 // One LM decision on the trial of one damping candidate.  Candidates are decided in
@@ -559,6 +565,9 @@ __device__ bool gn_decide(const DecideArgs& A) {
     }
   }
   c->done = done;
+  c->cands++;
+  if (first) c->rounds++;
+  if (c->accept && !done) c->lins++;
   if (A.gate) {  // [0]: rejected, [3]: finished -> trial_skipped
     A.gate[0] = !c->accept;
     A.gate[3] = done;
@@ -586,7 +595,17 @@ __device__ bool gn_decide(const DecideArgs& A) {
 // whole block
 __device__ void decide_block(const DecideArgs& A) {
   __shared__ int acc;
-  if (threadIdx.x == 0) acc = gn_decide(A) && A.ctl->accept;
+  if (threadIdx.x == 0) {
+    const bool decided = gn_decide(A);
+    acc = decided && A.ctl->accept;
+    if (A.graph && decided) {
+      const Control* c = A.ctl;
+      const int go_next = !c->accept && !c->done;
+      for (int m = A.cand + 1; m < A.nspec; ++m) cudaGraphSetConditional(A.h_cand[m], m == A.cand + 1 ? go_next : 0);
+      cudaGraphSetConditional(A.h_lin, c->accept && !c->done);
+      cudaGraphSetConditional(A.h_loop, !c->done);
+    }
+  }
   __syncthreads();
   if (acc) {
     for (int x = threadIdx.x; x < A.pose_words; x += blockDim.x) A.poses_dst[x] = A.poses_src[x];

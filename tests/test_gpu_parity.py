@@ -250,3 +250,22 @@ def test_damping_candidates_bitwise(torch_cuda, name, kf, calib):
         assert (r.trials, r.iterations_run, r.converged) == (r1.trials, r1.iterations_run, r1.converged)
         assert r.final_energy == r1.final_energy and r.lambda_final == r1.lambda_final
         assert list(r.energy_trace) == list(r1.energy_trace)
+
+
+def test_loop_graph_matches_stream_path(torch_cuda, monkeypatch):
+    """DBA_GRAPH=1 runs dba_solve's LM loop as one CUDA graph (WHILE over rounds, IF
+    nodes for later damping candidates and the linearisation); it must reproduce the
+    stream path bit for bit, rejections included."""
+    from paper_2411_17660_b200 import dba, scenes
+    wl = scenes.make_workload("C3", height=24, width=32, keyframes=64)
+    s = dba.DBASolver(wl.ii, wl.jj, len(wl.frames), 24, 32, wl.fixed)
+    outs = []
+    for g in ("0", "1", "1"):  # the second graph run reuses the instantiated graph
+        monkeypatch.setenv("DBA_GRAPH", g)
+        Po, Do, Ko, rep = s.solve(wl.poses0, wl.disps0, wl.intr0, wl.flow, iters=12)
+        outs.append((Po.cpu().numpy(), Do.cpu().numpy(), rep))
+    P0, D0, r0 = outs[0]
+    assert r0.trials > r0.iterations_run  # rejections exercised
+    for P, D, r in outs[1:]:
+        assert np.array_equal(P, P0) and np.array_equal(D, D0)
+        assert (r.trials, r.iterations_run, r.final_energy) == (r0.trials, r0.iterations_run, r0.final_energy)
