@@ -1019,11 +1019,12 @@ int launch_energy(Ctx& c, int slot, bool decide, int* status, bool from_epass = 
   f.energy_out = c.at<double>(p->L.sys[slot]) + p->energy_off;
   const bool multi = c.comm && p->nranks > 1;
   if (decide && !multi) {
-    if (int s = launch(c, finalize_decide_kernel, dim3(1), dim3(256), 0, false, f, decide_args(c, cand))) return s;
+    if (int s = launch(c, finalize_decide_kernel, dim3(1), dim3(kFinalThreads), 0, false, f, decide_args(c, cand)))
+      return s;
     mark(c, "fin+decide");
     return DBA_OK;
   }
-  if (int s = launch(c, finalize_kernel, dim3(1), dim3(256), 0, false, f)) return s;
+  if (int s = launch(c, finalize_kernel, dim3(1), dim3(kFinalThreads), 0, false, f)) return s;
   mark(c, "finalize");
   if (multi) {
     if (!nccl().ok) return DBA_ENCCL;

@@ -383,21 +383,27 @@ struct FinalArgs {
 };
 
 
+// fixed-order sum of the partial rows: strided per-thread sums, warp butterfly, then
+// the warp sums in order (kFinalThreads threads)
+constexpr int kFinalThreads = 1024;
 __device__ __forceinline__ void finalize_energy(const FinalArgs& A) {
-  __shared__ double sh[256];
+  __shared__ double sh[kFinalThreads / 32];
   double s = 0.0;
-#pragma unroll 8
-  for (int x = threadIdx.x; x < A.n; x += 256) s += A.part_frame[(long long)x * A.stride];
-  sh[threadIdx.x] = s;
+#pragma unroll 4
+  for (int x = threadIdx.x; x < A.n; x += kFinalThreads) s += A.part_frame[(long long)x * A.stride];
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = s;
   __syncthreads();
-  for (int off = 128; off >= 1; off >>= 1) {
-    if ((int)threadIdx.x < off) sh[threadIdx.x] += sh[threadIdx.x + off];
-    __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+#pragma unroll
+    for (int w = 0; w < kFinalThreads / 32; ++w) t += sh[w];
+    A.energy_out[0] = t;
   }
-  if (threadIdx.x == 0) A.energy_out[0] = sh[0];
 }
 
-__global__ void __launch_bounds__(256) finalize_kernel(const FinalArgs A) {
+__global__ void __launch_bounds__(kFinalThreads) finalize_kernel(const FinalArgs A) {
   pdl_enter();
   if (trial_skipped(A.status)) return;
   finalize_energy(A);
@@ -507,11 +513,14 @@ struct DecideArgs {
 // trials.  Returns false when the candidate was not needed (no state change beyond
 // propagating the skip).
 __device__ bool gn_decide(const DecideArgs& A) {
-  Control* c = A.ctl;
+  Control* cg = A.ctl;
   int* st = A.status;
   int* lp = A.loop;
   const bool first = st == lp;
-  if (lp[3] != 0 || (!first && st[3] != 0)) {  // finished, or an earlier candidate decided
+  // flags and controller scalars are read once into registers (the flags words may
+  // alias nothing in Control, but the compiler cannot know): one round of loads
+  const int s0 = st[0], s1 = st[1], s3 = st[3], l3 = lp[3];
+  if (l3 != 0 || (!first && s3 != 0)) {  // finished, or an earlier candidate decided
     if (!first) {
       st[0] = 0;
       st[1] = INT_MAX;
@@ -524,62 +533,73 @@ __device__ bool gn_decide(const DecideArgs& A) {
     }
     return false;
   }
-  c->accept = 0;
-  int done = 0;
-  if (st[0] != 0) {  // factorisation failed: more damping, same iterate
-    c->lam *= 10.0;
-    if (c->lam > A.lam_max) {
-      c->result = 1;  // DBA_ESOLVER (mapped by the host)
+  double lam = cg->lam, Ec = cg->Ec, cond = cg->cond;
+  int it = cg->it, trials = cg->trials, result = cg->result, converged = cg->converged;
+  int bad_edge = cg->bad_edge;
+  const double E = *A.energy;
+  const double cin = *A.cond;
+  int accept = 0, done = 0;
+  if (s0 != 0) {  // factorisation failed: more damping, same iterate
+    lam *= 10.0;
+    if (lam > A.lam_max) {
+      result = 1;  // DBA_ESOLVER (mapped by the host)
       done = 1;
     }
   } else {
-    c->trials++;
-    const double E = *A.energy;
+    trials++;
     if (A.calib) {
-      c->cond = *A.cond;
-      if (A.cond_max > 0.0 && c->cond > A.cond_max) {
-        c->result = 2;  // DBA_ECALIB
+      cond = cin;
+      if (A.cond_max > 0.0 && cond > A.cond_max) {
+        result = 2;  // DBA_ECALIB
         done = 1;
       }
     }
-    if (!done && (st[1] != INT_MAX || !isfinite(E))) {
-      c->bad_edge = st[1] != INT_MAX ? st[1] : -1;
-      c->result = 3;  // DBA_ENONFINITE
+    if (!done && (s1 != INT_MAX || !isfinite(E))) {
+      bad_edge = s1 != INT_MAX ? s1 : -1;
+      result = 3;  // DBA_ENONFINITE
       done = 1;
     }
     if (!done) {
-      if (E <= c->Ec) {
-        c->accept = 1;
-        c->Ec = E;
-        c->lam = fmax(c->lam / 10.0, A.lam_min);
-        if (c->it < kTraceMax) c->trace[c->it] = E;
-        c->it++;
-        if (c->it >= A.iters) done = 1;
+      if (E <= Ec) {
+        accept = 1;
+        Ec = E;
+        lam = fmax(lam / 10.0, A.lam_min);
+        if (it < kTraceMax) cg->trace[it] = E;
+        it++;
+        if (it >= A.iters) done = 1;
       } else {
-        c->lam *= 10.0;
-        if (c->lam > A.lam_max) {
-          c->converged = 1;
+        lam *= 10.0;
+        if (lam > A.lam_max) {
+          converged = 1;
           done = 1;
         }
       }
     }
   }
-  c->done = done;
-  c->cands++;
-  if (first) c->rounds++;
-  if (c->accept && !done) c->lins++;
+  cg->lam = lam;
+  cg->Ec = Ec;
+  cg->cond = cond;
+  cg->it = it;
+  cg->trials = trials;
+  cg->result = result;
+  cg->converged = converged;
+  cg->bad_edge = bad_edge;
+  cg->accept = accept;
+  cg->done = done;
+  cg->cands++;
+  if (first) cg->rounds++;
+  if (accept && !done) cg->lins++;
   if (A.gate) {  // [0]: rejected, [3]: finished -> trial_skipped
-    A.gate[0] = !c->accept;
+    A.gate[0] = !accept;
     A.gate[3] = done;
   }
   st[0] = 0;
   st[1] = INT_MAX;
   st[2] = 0;
-  if (first) st[3] = done;
-  else st[3] = 0;
+  st[3] = first ? done : 0;
   lp[3] = done;
   if (A.next) {  // the next candidate runs only after a rejection / failure
-    const int skip = c->accept || done;
+    const int skip = accept || done;
     A.next[3] = skip;
     A.next[1] = INT_MAX;
     if (skip) {
@@ -619,7 +639,7 @@ __global__ void decide_kernel(const DecideArgs A) {
 }
 
 // single rank: the trial energy and the LM decision in one launch
-__global__ void __launch_bounds__(256) finalize_decide_kernel(const FinalArgs F, const DecideArgs D) {
+__global__ void __launch_bounds__(kFinalThreads) finalize_decide_kernel(const FinalArgs F, const DecideArgs D) {
   pdl_enter();
   if (!trial_skipped(F.status)) finalize_energy(F);  // uniform over the block
   decide_block(D);
