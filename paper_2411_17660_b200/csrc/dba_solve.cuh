@@ -328,11 +328,7 @@ __device__ inline void chain_forward(const ChainSm& S, const double* band, doubl
       }
       CRIT_MARK(3);
     } else if (trail) {
-#ifdef DBA_SOLVE_NOSTAGE
-      const bool stage = false;  // timing experiment (results invalid)
-#else
       const bool stage = warp == kStageWarp && band != nullptr && b + BW + 1 < nrows;
-#endif
       if (stage) {
         // copy row b+BW+1 into row b's slot (free during step b)
         const char* src = reinterpret_cast<const char*>(band + (size_t)(b + BW + 1) * NR);
@@ -383,11 +379,7 @@ __device__ inline void chain_forward(const ChainSm& S, const double* band, doubl
       const int n2 = calib ? na * 4 : 0;
       const int n3 = calib ? 4 : 0;
       const int n4 = 6 * (na > 0 ? na - 1 : 0) + (calib ? 4 : 0);
-#ifdef DBA_SOLVE_NOTRAIL
-      const int ntot = 0;  // timing experiment: critical warp without the trailing traffic
-#else
       const int ntot = n1 + n2 + n3 + n4;
-#endif
       for (int x = gt; x < ntot; x += kTrailThreads) {
         if (x < n1) {
           const int pidx = x / (6 / kTR), rr = kTR * (x % (6 / kTR));
