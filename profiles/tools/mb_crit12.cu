@@ -1,0 +1,111 @@
+// single-warp replica of a 12x12-pivot critical step: 12 lanes (row each) form
+// L = S1 D^-1 and S11 -= L S1^T, lane 0 inverts the 12x12 block via 2x2 blocks of 6x6
+#include <cstdio>
+#include "../../paper_2411_17660_b200/csrc/dba_solve.cuh"
+using namespace dba;
+__device__ void inv12(const double* S, double* Di) {
+  // [A B; B^T C] with 6x6 blocks: Ai = inv6(A); T = Ai B; Cs = C - B^T T; Ci = inv6(Cs)
+  double A[36], Ai[36], B[36], T[36], Cs[36], Ci[36];
+  for (int r = 0; r < 6; ++r)
+    for (int c = 0; c < 6; ++c) {
+      A[6 * r + c] = S[12 * r + c];
+      B[6 * r + c] = S[12 * r + c + 6];
+      Cs[6 * r + c] = S[12 * (r + 6) + c + 6];
+    }
+  inv6_spd(A, 0.0, Ai);
+  for (int r = 0; r < 6; ++r)
+    for (int c = 0; c < 6; ++c) {
+      double s = 0;
+      for (int k = 0; k < 6; ++k) s = fma(Ai[6 * r + k], B[6 * k + c], s);
+      T[6 * r + c] = s;
+    }
+  for (int r = 0; r < 6; ++r)
+    for (int c = 0; c < 6; ++c) {
+      double s = Cs[6 * r + c];
+      for (int k = 0; k < 6; ++k) s = fma(-B[6 * k + r], T[6 * k + c], s);
+      Cs[6 * r + c] = s;
+    }
+  inv6_spd(Cs, 0.0, Ci);
+  for (int r = 0; r < 6; ++r)
+    for (int c = 0; c < 6; ++c) {
+      double u = 0;  // U = T Ci
+      for (int k = 0; k < 6; ++k) u = fma(T[6 * r + k], Ci[6 * k + c], u);
+      Di[12 * r + c + 6] = -u;
+      Di[12 * (c + 6) + r] = -u;
+      Di[12 * (r + 6) + c + 6] = Ci[6 * r + c];
+    }
+  for (int r = 0; r < 6; ++r)
+    for (int c = 0; c < 6; ++c) {
+      double s = Ai[6 * r + c];
+      for (int k = 0; k < 6; ++k) s = fma(-Di[12 * r + k + 6], T[6 * c + k], s);
+      Di[12 * r + c] = s;
+    }
+}
+template <int MODE>
+__global__ void k(double* out, long long* cyc, int n) {
+  __shared__ __align__(16) double S1[148], S11[148], dinv[288], z[24];
+  const int lane = threadIdx.x & 31;
+  for (int x = threadIdx.x; x < 144; x += blockDim.x) {
+    const int r = x / 12, c = x % 12;
+    S1[x] = 0.01 * (r + 2 * c);
+    S11[x] = (r == c ? 10.0 : 0.0) + 1.0 / (1 + r + c);
+    dinv[x] = (r == c ? 0.1 : 0.0);
+    dinv[144 + x] = (r == c ? 0.1 : 0.0);
+  }
+  if (threadIdx.x < 24) z[threadIdx.x] = 1.0;
+  __syncthreads();
+  if (threadIdx.x >= 32) return;
+  long long t0 = clock64(), tl = 0, ti = 0;
+  for (int b = 0; b < n; ++b) {
+    const double* Db = dinv + 144 * (b & 1);
+    long long ta = clock64();
+    if (MODE != 1 && lane < 12) {
+      const int r = lane;
+      double Lr[12];
+#pragma unroll
+      for (int c = 0; c < 12; ++c) Lr[c] = 0.0;
+#pragma unroll
+      for (int kk = 0; kk < 12; ++kk) {
+        const double sk = S1[12 * r + kk];
+#pragma unroll
+        for (int c = 0; c < 12; ++c) Lr[c] = fma(sk, Db[12 * kk + c], Lr[c]);
+      }
+      double d[12], zs = z[12 + r];
+#pragma unroll
+      for (int c = 0; c < 12; ++c) d[c] = S11[12 * r + c];
+#pragma unroll
+      for (int kk = 0; kk < 12; ++kk) {
+#pragma unroll
+        for (int c = 0; c < 12; ++c) d[c] = fma(-Lr[kk] * 1e-9, S1[12 * c + kk], d[c]);
+        zs = fma(-Lr[kk], z[kk], zs);
+      }
+#pragma unroll
+      for (int c = 0; c < 12; ++c) S11[12 * r + c] = d[c];
+      z[12 + r] = zs * 1e-9;
+    }
+    __syncwarp();
+    long long tb = clock64();
+    if (MODE != 2 && lane == 0) {
+      double* Dn = dinv + 144 * ((b + 1) & 1);
+      inv12(S11, Dn);
+    }
+    __syncwarp();
+    long long tc = clock64();
+    tl += tb - ta;
+    ti += tc - tb;
+  }
+  if (lane == 0) {
+    cyc[0] = clock64() - t0;
+    cyc[1] = tl;
+    cyc[2] = ti;
+    out[0] = dinv[0];
+  }
+}
+int main() {
+  double* o; long long* c; cudaMalloc(&o, 8); cudaMalloc(&c, 24);
+  for (int r = 0; r < 2; ++r) {
+    k<0><<<1, 64>>>(o, c, 1000); long long h[3]; cudaMemcpy(h, c, 24, cudaMemcpyDeviceToHost);
+    printf("12x12 step %.0f  L/S11 %.0f  inv %.0f cycles\n", h[0] / 1000.0, h[1] / 1000.0, h[2] / 1000.0);
+  }
+  printf("err %s\n", cudaGetErrorString(cudaGetLastError()));
+}
