@@ -231,7 +231,8 @@ def test_sharded_partial_systems_sum_to_full(torch_cuda, nranks):
     assert abs(es - e) <= 1e-10 * e
 
 
-@pytest.mark.parametrize("name,kf,calib", [("C1", None, False), ("C3", 64, False), ("C5", 60, True)])
+@pytest.mark.parametrize("name,kf,calib", [("C1", None, False), ("C3", 64, False), ("C4", None, False),
+                                           ("C5", 60, True)])
 def test_damping_candidates_bitwise(torch_cuda, name, kf, calib):
     """Speculative damping (lambda, 10 lambda, 100 lambda factored in one round) must
     reproduce the one-trial-at-a-time schedule exactly: same decisions, trial count,
@@ -239,10 +240,12 @@ def test_damping_candidates_bitwise(torch_cuda, name, kf, calib):
     trials are rejected."""
     from paper_2411_17660_b200 import dba, scenes
     wl = scenes.make_workload(name, height=24, width=32, keyframes=kf)
-    s = dba.DBASolver(wl.ii, wl.jj, len(wl.frames), 24, 32, wl.fixed, optimize_intrinsics=calib)
+    prior = wl.prior is not None
+    s = dba.DBASolver(wl.ii, wl.jj, len(wl.frames), 24, 32, wl.fixed, optimize_intrinsics=calib, use_prior=prior)
+    kw = dict(prior=wl.prior, prior_mask=wl.prior_mask) if prior else {}
     outs = []
     for nc in (1, 2, 3):
-        Po, Do, Ko, rep = s.solve(wl.poses0, wl.disps0, wl.intr0, wl.flow, iters=12, damping_candidates=nc)
+        Po, Do, Ko, rep = s.solve(wl.poses0, wl.disps0, wl.intr0, wl.flow, iters=12, damping_candidates=nc, **kw)
         outs.append((Po.cpu().numpy(), Do.cpu().numpy(), Ko.cpu().numpy(), rep))
     P1, D1, K1, r1 = outs[0]
     for P, D, K, r in outs[1:]:
