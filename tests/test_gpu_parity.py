@@ -272,3 +272,38 @@ def test_loop_graph_matches_stream_path(torch_cuda, monkeypatch):
     for P, D, r in outs[1:]:
         assert np.array_equal(P, P0) and np.array_equal(D, D0)
         assert (r.trials, r.iterations_run, r.final_energy) == (r0.trials, r0.iterations_run, r0.final_energy)
+
+
+def test_full_size_c3_properties(torch_cuda):
+    """BASELINE configs[2] at full size (300 keyframes, 2970 edges, 48x64), where the float64
+    oracle is too slow to run: size-independent properties of the 8-iteration solve -- a
+    non-increasing accepted-energy trace, a 1e9x energy reduction, finite outputs, the fixed
+    pose untouched, bit-identical repeat runs, and convergence to the synthetic scene's truth
+    (camera centres up to the monocular scale)."""
+    from paper_2411_17660_b200 import dba, scenes
+    from paper_2411_17660_b200 import geometry as geo
+    wl = scenes.make_workload("C3", height=48, width=64)
+    s = dba.DBASolver(wl.ii, wl.jj, len(wl.frames), 48, 64, wl.fixed)
+    Po, Do, Ko, rep = s.solve(wl.poses0, wl.disps0, wl.intr0, wl.flow, iters=8)
+    P, D = Po.cpu().numpy(), Do.cpu().numpy()
+    assert rep.iterations_run == 8
+    tr = [rep.initial_energy] + list(rep.energy_trace)
+    assert all(b <= a for a, b in zip(tr, tr[1:]))
+    assert rep.final_energy < 1e-9 * rep.initial_energy
+    assert np.isfinite(P).all() and np.isfinite(D).all() and (D > 0).all()
+    assert np.array_equal(P[0], wl.poses0[0])
+    P2, D2, _, rep2 = s.solve(wl.poses0, wl.disps0, wl.intr0, wl.flow, iters=8)
+    assert np.array_equal(P2.cpu().numpy(), P) and np.array_equal(D2.cpu().numpy(), D)
+    assert rep2.trials == rep.trials
+    # camera centres c = -R^T t of the world-to-camera poses vs truth, best common scale
+    def centres(poses):
+        out = []
+        for p in poses:
+            inv = geo.pose_inv(np.asarray(p, np.float64))
+            out.append(inv[4:])
+        return np.stack(out)
+    ce, ct = centres(P), centres(wl.true_poses)
+    ce, ct = ce - ce[0], ct - ct[0]
+    sc = float(np.sum(ce * ct) / np.sum(ce * ce))
+    err = np.linalg.norm(sc * ce - ct, axis=1).max() / np.linalg.norm(ct, axis=1).max()
+    assert err < 1e-4, err
