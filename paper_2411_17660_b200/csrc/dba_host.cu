@@ -1382,9 +1382,9 @@ int dba_solve(dba_plan* p, const dba_options* o, const dba_buffers* b, dba_repor
   }
   double Ec = rb.energy;
   rep->initial_energy = Ec;
-  // The whole LM schedule is enqueued without host round trips (decide_kernel);
-  // batches of trials are launched until the controller reports done.  Kernels of
-  // trials queued past the end return at entry.
+  // The whole LM schedule is enqueued without host round trips (the decision kernels);
+  // batches of rounds are launched until the controller reports done.  Kernels of
+  // rounds queued past the end return at entry.
   if ((s = upload_control(c, o->lambda0, Ec))) return rep->status = s;
   Control ctl{};
   ctl.lam = o->lambda0;
