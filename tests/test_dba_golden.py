@@ -1,0 +1,91 @@
+"""Committed DBA golden fixtures (tests/golden/dba_*.npz, made by make_dba_golden.py from
+the float64 oracle): the oracle is pinned against them on CPU, the GPU path is compared to
+them per config and per GN iteration (SURVEY §8c/§8d parity bar: 1e-4 relative on every
+disparity and pose translation)."""
+
+from __future__ import annotations
+
+import os
+
+import numpy as np
+import pytest
+
+from oracle import dba as O
+from paper_2411_17660_b200 import scenes
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+TAGS = ["C1", "C2", "C4", "C5"]
+REL_TOL = 1e-4
+# Documented exception (DESIGN.md §5 "Parity at C4"): with the depth prior the monocular scale
+# is fixed only by alpha = 1e-3 (reduced system condition 1.3e8 at 48x64), and the fp32
+# per-pixel assembly moves the FIRST step along that direction by ~3e-4 relative (uniform
+# disparity scale 1.0001, max 4.1e-4); the second iteration is back inside 1e-4 (2.8e-5).
+DISP_TOL = {("C4", 1): 5e-4}
+
+
+def _load(tag):
+    return np.load(os.path.join(GOLD, f"dba_{tag}.npz"))
+
+
+def _workload(g):
+    kf = int(g["keyframes"])
+    cfg = str(g["config"])
+    base = scenes.CONFIGS[cfg]["keyframes"]
+    return scenes.make_workload(cfg, height=int(g["height"]), width=int(g["width"]),
+                                keyframes=None if kf == base else kf)
+
+
+def _checksum(wl):
+    h = np.float64(0.0)
+    for a in (wl.poses0, wl.disps0, wl.flow, wl.intr0):
+        x = np.asarray(a, np.float64).ravel()
+        h += np.sum(x * (1.0 + np.arange(x.size) % 7))
+    return float(h)
+
+
+@pytest.mark.parametrize("tag", TAGS)
+def test_fixture_inputs_match_workload(tag):
+    g = _load(tag)
+    wl = _workload(g)
+    assert _checksum(wl) == float(g["checksum"])
+
+
+def test_oracle_reproduces_c1_fixture():
+    g = _load("C1")
+    wl = _workload(g)
+    prob = O.Problem(ii=wl.ii, jj=wl.jj, flow=wl.flow, fixed=wl.fixed)
+    st = O.State(wl.poses0.astype(np.float64).copy(), wl.disps0.astype(np.float64).copy(),
+                 wl.intr0.astype(np.float64).copy())
+    res, rep = O.solve(st, prob, O.Options(iters=1))
+    assert np.allclose(res.poses, g["poses_1"], rtol=1e-12, atol=1e-14)
+    assert np.allclose(res.disps.astype(np.float32), g["disps_1"], rtol=1e-6, atol=0)
+    assert np.allclose(rep.energy_trace, g["energy_1"], rtol=1e-12)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("tag", TAGS)
+def test_gpu_matches_fixture_per_iteration(tag):
+    import torch
+    from paper_2411_17660_b200 import dba
+    from tests.helpers import pose_errors
+    if not torch.cuda.is_available():
+        pytest.fail("GPU tests require a CUDA device")
+    g = _load(tag)
+    wl = _workload(g)
+    calib, prior = bool(g["calib"]), bool(g["prior"])
+    H, W = int(g["height"]), int(g["width"])
+    s = dba.DBASolver(wl.ii, wl.jj, len(wl.frames), H, W, wl.fixed, optimize_intrinsics=calib, use_prior=prior)
+    kw = dict(prior=wl.prior, prior_mask=wl.prior_mask) if prior else {}
+    for n in range(1, int(g["iters"]) + 1):
+        Po, Do, Ko, rep = s.solve(wl.poses0, wl.disps0, wl.intr0, wl.flow, iters=n, **kw)
+        assert rep.iterations_run == len(g[f"energy_{n}"])
+        te, ae = pose_errors(Po.cpu().numpy(), g[f"poses_{n}"])
+        assert te < REL_TOL, (tag, n, te)
+        assert ae < 1e-3, (tag, n, ae)
+        d, dr = Do.cpu().numpy().astype(np.float64), g[f"disps_{n}"].astype(np.float64)
+        rel = np.abs(d - dr) / dr
+        assert rel.max() < DISP_TOL.get((tag, n), REL_TOL), (tag, n, rel.max(), np.quantile(rel, 0.999))
+        if calib:
+            assert np.max(np.abs(Ko.cpu().numpy() - g[f"intr_{n}"]) / g[f"intr_{n}"]) < REL_TOL
+        e_ref = g[f"energy_{n}"][-1]
+        assert abs(rep.final_energy - e_ref) <= REL_TOL * rep.initial_energy
