@@ -80,7 +80,7 @@ struct Readback {
 
 struct Layout {
   // metadata (uploaded once per workspace)
-  size_t csr_off, slot_flow, frame_of, slot_i, slot_j, slot_edge, ridx;
+  size_t csr_off, slot_flow, frame_of, slot_i, slot_j, slot_edge, ridx, block_pose;
   size_t seg_frame, seg_t0, seg_t1, seg_off_edge, seg_off_M, seg_off_w, cta_seg, frame_seg;
   size_t off_F, off_f, units, contrib, meta_end;
   // state
@@ -93,6 +93,7 @@ struct Layout {
 struct dba_plan {
   int N = 0, H = 0, W = 0, P = 0, E = 0;
   int calib = 0, prior = 0, freeze_d = 0, gauge_on = 0, gauge_frame = -1, rank = 0, nranks = 1;
+  int scalefix = 0, anchor = -1;  // prior-fixed monocular scale: exact-row step correction
   int f0 = 0, f1 = 0, NL = 0, EL = 0, kmax = 0, nb = 0, BW = 0, n_red = 0;
   int n_tiles = 0, G = 0, nseg = 0, n_units = 0, nve = kEdgeVals, stage = 1;
   size_t pass_smem = 0, solve_smem = 0;
@@ -111,9 +112,10 @@ struct dba_plan {
     cudaGraphConditionalHandle h_loop = 0, h_lin = 0, h_cand[kMaxSpec] = {};
     int nodes_round = 0, nodes_cand = 0, nodes_lin = 0;  // kernels per segment (launch accounting)
   } lg;
-  long long band_len = 0, rband_off = 0, theta_off = 0, thth_off = 0, y_off = 0, energy_off = 0;
+  long long band_len = 0, rband_off = 0, theta_off = 0, thth_off = 0, y_off = 0, q_off = 0, energy_off = 0;
   int two_sided = 0, m_top = 0;  // two-CTA solve: pivots of the top chain
   std::vector<int> fixed_ridx;
+  std::vector<int> block_pose;  // reduced block -> pose
   std::vector<int> local_edges;  // input edge id of each local flow row
   Layout L{};
   std::vector<unsigned char> meta;  // image of [0, meta_end)
@@ -244,6 +246,12 @@ int dba_plan_create(const dba_problem_desc* d, dba_plan** out) {
   for (int k = 0; k < N && p->gauge_frame < 0; ++k)
     if (d->fixed[k]) p->gauge_frame = k;
   if (!gauge) p->gauge_frame = -1;
+  // with a depth prior and one fixed pose the monocular scale is fixed only by alpha: the
+  // reduced system has one weak direction u (scaling about the anchor camera) whose row S u
+  // is formed exactly and used to correct the step (DESIGN.md §5 "Parity at C4")
+  p->scalefix = (nfixed == 1 && p->prior && !p->freeze_d && !gauge && d->nranks <= 1) ? 1 : 0;
+  for (int k = 0; k < N && p->anchor < 0; ++k)
+    if (d->fixed[k]) p->anchor = k;
 
   // ---- partition + local CSR (stable by source frame)
   std::vector<int> bounds;
@@ -293,6 +301,9 @@ int dba_plan_create(const dba_problem_desc* d, dba_plan** out) {
     if (!d->fixed[k]) p->fixed_ridx[k] = nfree++;
   p->nb = nfree;
   p->n_red = 6 * nfree + 4 * p->calib;
+  p->block_pose.assign(std::max(nfree, 1), 0);
+  for (int k = 0; k < N; ++k)
+    if (p->fixed_ridx[k] >= 0) p->block_pose[p->fixed_ridx[k]] = k;
   // band width from the fill-in pattern of every source frame
   std::vector<std::vector<int>> vars(N);
   for (int k = 0; k < N; ++k) vars[k].push_back(k);
@@ -321,7 +332,8 @@ int dba_plan_create(const dba_problem_desc* d, dba_plan** out) {
   p->theta_off = p->band_len * (p->two_sided ? 2 : 1);
   p->thth_off = p->theta_off + (long long)p->nb * 24;
   p->y_off = p->thth_off + 16;
-  p->energy_off = p->y_off + p->n_red;
+  p->q_off = p->y_off + p->n_red;
+  p->energy_off = p->q_off + (p->scalefix ? p->n_red : 0);
   p->sys_len = (p->energy_off + 1 + 3) & ~3LL;
 
   // ---- solve kernel shared memory
@@ -411,7 +423,7 @@ int dba_plan_create(const dba_problem_desc* d, dba_plan** out) {
     off_F[fl] = nF;
     nF += (long long)m * m;
     off_f[fl] = nF;
-    nF += m;
+    nF += m * (p->scalefix ? 2 : 1);  // f, then (scalefix) the scale-direction row q
   }
 
   // ---- deterministic gather lists for the packed reduced system
@@ -537,6 +549,38 @@ int dba_plan_create(const dba_problem_desc* d, dba_plan** out) {
       u.c1 = (int)contrib.size();
       units.push_back(u);
     }
+    if (p->scalefix) {  // q: the same lists as y, from the row stored after each f
+      for (int a = 0; a < p->nb; ++a) {
+        GatherUnit u;
+        u.dst = p->q_off + 6LL * a;
+        u.rows = 6;
+        u.cols = 1;
+        u.c0 = (int)contrib.size();
+        for (int fl = 0; fl < p->NL; ++fl) {
+          const int m = mdim(fl);
+          if (m == 0) continue;
+          const int ra = local_row(fl, pose_of_block[a]);
+          if (ra < 0) continue;
+          contrib.push_back({off_f[fl] + m + ra, 1, 0});
+        }
+        u.c1 = (int)contrib.size();
+        units.push_back(u);
+      }
+      if (p->calib) {
+        GatherUnit u;
+        u.dst = p->q_off + 6LL * p->nb;
+        u.rows = 4;
+        u.cols = 1;
+        u.c0 = (int)contrib.size();
+        for (int fl = 0; fl < p->NL; ++fl) {
+          const int m = mdim(fl);
+          if (m == 0) continue;
+          contrib.push_back({off_f[fl] + m + (m - 4), 1, 0});
+        }
+        u.c1 = (int)contrib.size();
+        units.push_back(u);
+      }
+    }
   }
   p->n_units = (int)units.size();
 
@@ -555,6 +599,7 @@ int dba_plan_create(const dba_problem_desc* d, dba_plan** out) {
   L.slot_j = take(sizeof(int) * slot_j.size());
   L.slot_edge = take(sizeof(int) * slot_edge.size());
   L.ridx = take(sizeof(int) * N);
+  L.block_pose = take(sizeof(int) * p->block_pose.size());
   L.seg_frame = take(sizeof(int) * seg_frame.size());
   L.seg_t0 = take(sizeof(int) * seg_t0.size());
   L.seg_t1 = take(sizeof(int) * seg_t1.size());
@@ -607,6 +652,7 @@ int dba_plan_create(const dba_problem_desc* d, dba_plan** out) {
   put(p->meta, L.slot_j, slot_j);
   put(p->meta, L.slot_edge, slot_edge);
   put(p->meta, L.ridx, p->fixed_ridx);
+  put(p->meta, L.block_pose, p->block_pose);
   put(p->meta, L.seg_frame, seg_frame);
   put(p->meta, L.seg_t0, seg_t0);
   put(p->meta, L.seg_t1, seg_t1);
@@ -881,6 +927,7 @@ int launch_pass(Ctx& c, int cur, int nxt, bool backsub, bool system, bool gated 
   a.backsub = backsub ? 1 : 0;
   a.system = system ? 1 : 0;
   a.stage = p->stage;
+  a.scalefix = p->scalefix;
   a.status = gated ? gate_word(c) : c.at<int>(p->L.flags);
   a.runs = gated ? &c.at<Readback>(p->L.flags)->runs : nullptr;
   a.csr_off = c.at<int>(p->L.csr_off);
@@ -1064,6 +1111,7 @@ int launch_system(Ctx& c, int slot, bool decide = false, bool gated = false) {
     a.off_f = c.at<long long>(p->L.off_f);
     a.bad_edge = c.at<int>(p->L.flags) + 1;
     a.gauge_frame = p->gauge_on ? p->gauge_frame : -1;
+    a.scalefix = p->scalefix;
     a.frame_of = c.at<int>(p->L.frame_of);
     a.gstate = c.at<double>(p->L.gstate[slot]);
     const size_t smem = assemble_smem_bytes(std::max(p->kmax, 1), p->calib);
@@ -1116,6 +1164,13 @@ int launch_solve(Ctx& c, int slot, int nspec = 1) {
   a.delta = c.at<double>(p->L.delta);
   a.cond = &c.at<Readback>(p->L.flags)->cond;
   a.m_top = p->m_top;
+  a.scalefix = p->scalefix;
+  a.q = s + p->q_off;
+  a.poses = c.at<double>(p->L.poses[slot]);
+  a.block_pose = c.at<int>(p->L.block_pose);
+  a.anchor = p->anchor;
+  a.part_frame = c.at<double>(p->L.part_frame);
+  a.nseg = p->nseg;
   a.nspec = nspec;
   a.spec_Lband = p->spec_Lband;
   a.spec_rLband = p->spec_rLband;

@@ -49,6 +49,7 @@ struct PassArgs {
   int freeze;   // disparity block frozen (motion-only / pose stage): no Schur fill-in, d unchanged
   int system;   // produce system partials (0: energy only)
   int stage;    // flow records of the next sub-tile are staged in smem with cp.async
+  int scalefix; // prior-fixed monocular scale: the A5 column carries c = d (eta + alpha m) instead
   const int* status;  // see trial_skipped
   unsigned long long* runs;  // counts executed launches (profiling of gated passes) or null
   const int* csr_off;
@@ -282,6 +283,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) pass_kernel(const PassArgs A)
     float facc[15];  // energy, H_tt (10), g_t (4)
 #pragma unroll
     for (int x = 0; x < 15; ++x) facc[x] = 0.f;
+    float fpri = 0.f;  // scalefix: sum_p d_p alpha m_p (d*_p - d_p) (the prior's gradient along the scale)
     // A5: kappa = (rho - h . delta_local) / gamma from the x_c linearisation
     const bool gauge = (f == A.gauge_frame) && k > 0;
     __syncthreads();
@@ -536,13 +538,17 @@ __global__ void __launch_bounds__(kPassThreads, 1) pass_kernel(const PassArgs A)
           }
         }
         const float dn = dns[pl];
+        float ap = 0.f;
         if (A.prior != nullptr && in) {
           const size_t fp = (size_t)f * P + p;
-          const float ap = A.alpha * (A.pweight ? A.pweight[f] : 1.f) * (float)A.pmask[fp];
+          ap = A.alpha * (A.pweight ? A.pweight[f] : 1.f) * (float)A.pmask[fp];
           const float dd = A.prior[fp] - dn;
           C += ap;
           gd += ap * dd;
-          if (half == 0) facc[0] += ap * dd * dd;
+          if (half == 0) {
+            facc[0] += ap * dd * dd;
+            fpri = fmaf(dn * ap, dd, fpri);
+          }
         }
         if (A.system) {
           // V = U_ext / sqrt(C): the GEMM below is then M_ext = V V^T
@@ -563,7 +569,10 @@ __global__ void __launch_bounds__(kPassThreads, 1) pass_kernel(const PassArgs A)
               U2[ne] = make_float2(Et[0] * sq, Et[1] * sq);
               U2[ne + 1] = make_float2(Et[2] * sq, Et[3] * sq);
             }
-            U2[mu >> 1] = make_float2(gd * sq, in ? C / dn * sq : 0.f);  // A5 with c = C/d
+            // second extra column: A5 gauge c = C/d, or (scalefix) c = d (eta + alpha m), whose
+            // E C^-1 c is the reduced system's exact row along the monocular scale direction
+            const float cx = A.scalefix ? dn * (A.eta + ap) : C / dn;
+            U2[mu >> 1] = make_float2(gd * sq, in ? cx * sq : 0.f);
             for (int c = (mext >> 1); c < (mpad >> 1); ++c) U2[c] = make_float2(0.f, 0.f);
           }
         }
@@ -624,12 +633,20 @@ __global__ void __launch_bounds__(kPassThreads, 1) pass_kernel(const PassArgs A)
       for (int off = 16; off >= 1; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
       if (lane == 0) red[warp * 16 + x] = (double)v;
     }
+    {
+      double v = (double)fpri;
+#pragma unroll
+      for (int off = 16; off >= 1; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+      if (lane == 0) red[warp * 16 + 15] = v;
+    }
     __syncthreads();
     double* pf = A.part_frame + (long long)sg * kFrameVals;
     if (tid < kFrameVals) {
       double v = 0.0;
       if (tid < 15)
         for (int w = 0; w < kPassWarps; ++w) v += red[w * 16 + tid];
+      if (tid == 17)
+        for (int w = 0; w < kPassWarps; ++w) v += red[w * 16 + 15];
       pf[tid] = v;  // [15], [16] (gamma, rho) are overwritten below when system
     }
     if (A.system) {

@@ -68,6 +68,15 @@ struct SolveArgs {
   double* delta;        // 6 nb + 4 calib
   double* cond;         // theta pivot ratio
   int m_top;            // two-sided: pivots of the top chain (0: one-sided)
+  // prior-fixed monocular scale (DESIGN.md §5 "Parity at C4"): q = exact S u along the
+  // scaling u about the anchor camera; the step is corrected along u after the solve
+  int scalefix;
+  const double* q;
+  const double* poses;      // current poses (N,7)
+  const int* block_pose;    // reduced block -> pose
+  int anchor;
+  const double* part_frame;  // per-segment [.., 16] rho_c, [17] sum d alpha m (d* - d) (u.y exactly)
+  int nseg;
   // speculative damping: candidate k (one CTA / CTA pair each) factors S + 10^k lambda I
   // into its own factor rows, exchange scratch, step, flags word and condition slot,
   // so the trials a rejection would run next are already solved
@@ -701,6 +710,72 @@ __device__ inline ChainSm chain_sm(unsigned char* smem, const SolveSmem& L, int*
   return S;
 }
 
+// Step correction along the prior-fixed scale direction u (u_k = t_k - R_k R_0^T t_0 in the
+// translation slots, scaling about the anchor camera 0).  The fp32-assembled S is accurate
+// to ~5e-8 but that error lands on u, whose eigenvalue is ~alpha-sized; q = S u is formed
+// exactly (the flow terms cancel analytically), so with x the computed step:
+//   x += u (u.y - (q + lam u).x) / (u.q + lam u.u)
+// One CTA, after the whole step x is written.
+__device__ void scale_correct(const SolveArgs& A, double lam) {
+  __shared__ double red[5][kSolveThreads / 32];
+  __shared__ double beta_s;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const double* p0 = A.poses + 7 * (size_t)A.anchor;
+  double q0[4] = {p0[0], p0[1], p0[2], p0[3]};
+  quat_normalize(q0);
+  double R0[9];
+  quat_to_rot(q0, R0);
+  double c0[3];  // anchor camera centre -R0^T t0
+  for (int r = 0; r < 3; ++r) c0[r] = -(R0[r] * p0[4] + R0[3 + r] * p0[5] + R0[6 + r] * p0[6]);
+  // u.y exactly: the flow gradient has no component along u, so
+  //   u.y = sum_p d_p [(eta + alpha m_p) g_d,p - C_p g^prior_p] / C_p = sum_segments (rho - pi)
+  // with rho = c^T C^-1 g_d (c = d (eta + alpha m), the pass's GEMM) and pi the prior sum
+  double d[5] = {0.0, 0.0, 0.0, 0.0, 0.0};  // u.y, q.x, u.x, u.q, u.u
+  for (int sg = tid; sg < A.nseg; sg += kSolveThreads)
+    d[0] += A.part_frame[(size_t)sg * kFrameVals + 16] - A.part_frame[(size_t)sg * kFrameVals + 17];
+  for (int a = tid; a < A.nb; a += kSolveThreads) {
+    const double* pk = A.poses + 7 * (size_t)A.block_pose[a];
+    double qk[4] = {pk[0], pk[1], pk[2], pk[3]};
+    quat_normalize(qk);
+    double Rk[9];
+    quat_to_rot(qk, Rk);
+    for (int r = 0; r < 3; ++r) {
+      const double u = pk[4 + r] + (Rk[3 * r] * c0[0] + Rk[3 * r + 1] * c0[1] + Rk[3 * r + 2] * c0[2]);
+      const double x = A.delta[6 * a + r], q = A.q[6 * a + r];
+      d[2] += u * x;
+      d[3] += u * q;
+      d[4] += u * u;
+    }
+  }
+  for (int x = tid; x < A.nb * 6 + (A.calib ? 4 : 0); x += kSolveThreads) d[1] += A.q[x] * A.delta[x];
+  for (int i = 0; i < 5; ++i) {
+    double v = d[i];
+    for (int off = 16; off >= 1; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    if (lane == 0) red[i][warp] = v;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double t[5];
+    for (int i = 0; i < 5; ++i) {
+      t[i] = 0.0;
+      for (int w = 0; w < kSolveThreads / 32; ++w) t[i] += red[i][w];
+    }
+    const double den = t[3] + lam * t[4];
+    beta_s = den > 0.0 ? (t[0] - t[1] - lam * t[2]) / den : 0.0;
+  }
+  __syncthreads();
+  const double beta = beta_s;
+  for (int a = tid; a < A.nb; a += kSolveThreads) {
+    const double* pk = A.poses + 7 * (size_t)A.block_pose[a];
+    double qk[4] = {pk[0], pk[1], pk[2], pk[3]};
+    quat_normalize(qk);
+    double Rk[9];
+    quat_to_rot(qk, Rk);
+    for (int r = 0; r < 3; ++r)
+      A.delta[6 * a + r] += beta * (pk[4 + r] + (Rk[3 * r] * c0[0] + Rk[3 * r + 1] * c0[1] + Rk[3 * r + 2] * c0[2]));
+  }
+}
+
 // one-sided solve (small systems)
 template <int NS>
 __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const SolveArgs A0) {
@@ -733,6 +808,10 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const SolveArgs
   }
   chain_backward<NS>(S.z, S.thL, S.z + 6 * nb, A.Lband, S.ring, S.bars, nb, nb, BW, A.calib, A.delta);
   for (int x = tid; x < 6 * nb + (A.calib ? 4 : 0); x += kSolveThreads) A.delta[x] = S.z[x];
+  if (A.scalefix) {
+    __syncthreads();
+    scale_correct(A, lam);
+  }
 }
 
 // two-sided solve: 2 cooperative CTAs (see the header comment)
@@ -854,13 +933,14 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve2_kernel(const SolveArg
   }
   __threadfence();
   grid.sync();
-  if (*((volatile int*)gfail) != 0) {
-    if (tid == 0 && cta == 0) A.status[0] = 1;
-    return;
-  }
+  // a failed candidate skips its back-substitution but stays in the grid: the scale
+  // correction below needs one more grid-wide barrier
+  const bool failed = *((volatile int*)gfail) != 0;
+  if (failed && tid == 0 && cta == 0) A.status[0] = 1;
 #ifdef DBA_SOLVE_PROF
   long long ph2 = clock64();
 #endif
+  if (!failed) {
   // ---- back-substitute this chain with the middle solution
   for (int x = tid; x < 6 * BW; x += kSolveThreads) {
     const int i = x / 6, s = x % 6;  // local middle row npiv + i
@@ -877,6 +957,12 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve2_kernel(const SolveArg
   if (cta == 0) {
     for (int x = tid; x < 6 * BW; x += kSolveThreads) A.delta[6 * m + x] = xsol[x];
     if (calib && tid < 4) A.delta[6 * nb + tid] = xsol[6 * BW + tid];
+  }
+  }
+  if (A.scalefix) {
+    __threadfence();
+    grid.sync();  // both chains' steps are in A.delta
+    if (!failed && cta == 0) scale_correct(A, lam);
   }
 #ifdef DBA_SOLVE_PROF
   if (cta == 0 && tid == 0) {

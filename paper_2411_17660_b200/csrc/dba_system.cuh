@@ -149,6 +149,7 @@ struct AsmArgs {
   const long long* off_f;
   int* bad_edge;
   int gauge_frame;        // A5 (global frame id) or -1
+  int scalefix;           // write the frame's exact scale-direction row q after f
   const int* frame_of;
   double* gstate;         // out: [gamma, rho, h] for the gauge frame
 };
@@ -305,6 +306,22 @@ __global__ void __launch_bounds__(512) assemble_kernel(const AsmArgs A) {
         v = hs[(cu / 6) * nve + 21 + cu % 6] - ws[cu];
     }
     fv[x] = v;
+  }
+  if (A.scalefix) {
+    // exact S u along the prior-fixed monocular scale u (the flow terms cancel analytically):
+    // T h with h = E C^-1 c, c = d (eta + alpha m); stored after f for the gather
+    double* qv = fv + m;
+    for (int x = tid; x < m; x += blockDim.x) {
+      double v;
+      if (x < 6) {
+        v = 0.0;
+        for (int e = 0; e < k; ++e)
+          for (int q = 0; q < 6; ++q) v -= Ad[36 * e + 6 * q + x] * hg[6 * e + q];
+      } else {
+        v = hg[x - 6];
+      }
+      qv[x] = v;
+    }
   }
   if (!gauge) return;
   // A5 gauge constraint (Sherman-Morrison): F += (T h)(T h)^T / gamma, f += (T h) rho / gamma

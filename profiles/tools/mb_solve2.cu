@@ -40,7 +40,7 @@ int main(int argc, char** argv) {
   SolveArgs a; a.nb = nb; a.BW = BW; a.calib = 0; a.lambda = dlam; a.status = dst; a.band = dband; a.rband = drband;
   a.theta = dband; a.thth = dband; a.y = dy; a.Lband = dL; a.rLband = drL; a.mid = dmid; a.delta = ddel; a.cond = dcond;
   a.m_top = (nb - BW) / 2;
-  a.nspec = 1; a.spec_Lband = a.spec_rLband = a.spec_mid = a.spec_delta = 0;
+  a.nspec = 1; a.spec_Lband = a.spec_rLband = a.spec_mid = a.spec_delta = 0; a.scalefix = 0;
   for (int k = 0; k < kMaxSpec; ++k) { a.spec_status[k] = dst; a.spec_cond[k] = dcond; }
   SolveSmem s = solve_smem_layout(nb, BW, 0);
   cudaFuncSetAttribute(solve2_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s.total);
