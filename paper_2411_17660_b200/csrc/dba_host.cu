@@ -249,7 +249,7 @@ int dba_plan_create(const dba_problem_desc* d, dba_plan** out) {
   // with a depth prior and one fixed pose the monocular scale is fixed only by alpha: the
   // reduced system has one weak direction u (scaling about the anchor camera) whose row S u
   // is formed exactly and used to correct the step (DESIGN.md §5 "Parity at C4")
-  p->scalefix = (nfixed == 1 && p->prior && !p->freeze_d && !gauge && d->nranks <= 1) ? 1 : 0;
+  p->scalefix = (nfixed == 1 && p->prior && !p->freeze_d && !gauge) ? 1 : 0;
   for (int k = 0; k < N && p->anchor < 0; ++k)
     if (d->fixed[k]) p->anchor = k;
 
@@ -333,7 +333,7 @@ int dba_plan_create(const dba_problem_desc* d, dba_plan** out) {
   p->thth_off = p->theta_off + (long long)p->nb * 24;
   p->y_off = p->thth_off + 16;
   p->q_off = p->y_off + p->n_red;
-  p->energy_off = p->q_off + (p->scalefix ? p->n_red : 0);
+  p->energy_off = p->q_off + (p->scalefix ? p->n_red + 1 : 0);  // q, then u.y
   p->sys_len = (p->energy_off + 1 + 3) & ~3LL;
 
   // ---- solve kernel shared memory
@@ -423,7 +423,7 @@ int dba_plan_create(const dba_problem_desc* d, dba_plan** out) {
     off_F[fl] = nF;
     nF += (long long)m * m;
     off_f[fl] = nF;
-    nF += m * (p->scalefix ? 2 : 1);  // f, then (scalefix) the scale-direction row q
+    nF += p->scalefix ? 2 * m + 1 : m;  // f, then (scalefix) the scale-direction row q and u.y
   }
 
   // ---- deterministic gather lists for the packed reduced system
@@ -576,6 +576,20 @@ int dba_plan_create(const dba_problem_desc* d, dba_plan** out) {
           const int m = mdim(fl);
           if (m == 0) continue;
           contrib.push_back({off_f[fl] + m + (m - 4), 1, 0});
+        }
+        u.c1 = (int)contrib.size();
+        units.push_back(u);
+      }
+      {  // u.y: per-frame scalars after q, summed in frame order (partial per rank)
+        GatherUnit u;
+        u.dst = p->q_off + p->n_red;
+        u.rows = 1;
+        u.cols = 1;
+        u.c0 = (int)contrib.size();
+        for (int fl = 0; fl < p->NL; ++fl) {
+          const int m = mdim(fl);
+          if (m == 0) continue;
+          contrib.push_back({off_f[fl] + 2 * m, 1, 0});
         }
         u.c1 = (int)contrib.size();
         units.push_back(u);
@@ -1169,8 +1183,6 @@ int launch_solve(Ctx& c, int slot, int nspec = 1) {
   a.poses = c.at<double>(p->L.poses[slot]);
   a.block_pose = c.at<int>(p->L.block_pose);
   a.anchor = p->anchor;
-  a.part_frame = c.at<double>(p->L.part_frame);
-  a.nseg = p->nseg;
   a.nspec = nspec;
   a.spec_Lband = p->spec_Lband;
   a.spec_rLband = p->spec_rLband;

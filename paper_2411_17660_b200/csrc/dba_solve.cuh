@@ -75,8 +75,7 @@ struct SolveArgs {
   const double* poses;      // current poses (N,7)
   const int* block_pose;    // reduced block -> pose
   int anchor;
-  const double* part_frame;  // per-segment [.., 16] rho_c, [17] sum d alpha m (d* - d) (u.y exactly)
-  int nseg;
+
   // speculative damping: candidate k (one CTA / CTA pair each) factors S + 10^k lambda I
   // into its own factor rows, exchange scratch, step, flags word and condition slot,
   // so the trials a rejection would run next are already solved
@@ -727,12 +726,10 @@ __device__ void scale_correct(const SolveArgs& A, double lam) {
   quat_to_rot(q0, R0);
   double c0[3];  // anchor camera centre -R0^T t0
   for (int r = 0; r < 3; ++r) c0[r] = -(R0[r] * p0[4] + R0[3 + r] * p0[5] + R0[6 + r] * p0[6]);
-  // u.y exactly: the flow gradient has no component along u, so
-  //   u.y = sum_p d_p [(eta + alpha m_p) g_d,p - C_p g^prior_p] / C_p = sum_segments (rho - pi)
+  // u.y exactly (gathered after q): the flow gradient has no component along u, so
+  //   u.y = sum_p d_p [(eta + alpha m_p) g_d,p - C_p g^prior_p] / C_p = sum_frames (rho - pi)
   // with rho = c^T C^-1 g_d (c = d (eta + alpha m), the pass's GEMM) and pi the prior sum
-  double d[5] = {0.0, 0.0, 0.0, 0.0, 0.0};  // u.y, q.x, u.x, u.q, u.u
-  for (int sg = tid; sg < A.nseg; sg += kSolveThreads)
-    d[0] += A.part_frame[(size_t)sg * kFrameVals + 16] - A.part_frame[(size_t)sg * kFrameVals + 17];
+  double d[5] = {tid == 0 ? A.q[A.nb * 6 + (A.calib ? 4 : 0)] : 0.0, 0.0, 0.0, 0.0, 0.0};  // u.y, q.x, u.x, u.q, u.u
   for (int a = tid; a < A.nb; a += kSolveThreads) {
     const double* pk = A.poses + 7 * (size_t)A.block_pose[a];
     double qk[4] = {pk[0], pk[1], pk[2], pk[3]};

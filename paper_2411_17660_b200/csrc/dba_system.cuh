@@ -311,6 +311,8 @@ __global__ void __launch_bounds__(512) assemble_kernel(const AsmArgs A) {
     // exact S u along the prior-fixed monocular scale u (the flow terms cancel analytically):
     // T h with h = E C^-1 c, c = d (eta + alpha m); stored after f for the gather
     double* qv = fv + m;
+    // u.y of this frame: rho (= c^T C^-1 g_d with the scale column c) minus the prior sum
+    if (tid == 0) qv[m] = fs[16] - fs[17];
     for (int x = tid; x < m; x += blockDim.x) {
       double v;
       if (x < 6) {
