@@ -3,8 +3,8 @@
 
     python tests/golden/make_dba_golden.py
 
-For each BASELINE config family (C1 mono, C2 frontend window, C4 depth prior, C5 self-
-calibrating; C3 is covered at full size by property tests) the deterministic workload of
+For each BASELINE config (C1 mono, C2 frontend window, C3 global backend, C4 depth prior,
+C5 self-calibrating), at its own 48x64 resolution, the deterministic workload of
 ``paper_2411_17660_b200.scenes.make_workload`` is solved by ``oracle.dba.solve`` for
 1..iters accepted GN iterations, and the state after each is stored (poses and
 intrinsics float64, disparities float32 -- 6e-8 relative, far below the 1e-4 bar), with
@@ -32,8 +32,9 @@ from paper_2411_17660_b200 import scenes  # noqa: E402
 FIXTURES = {
     "C1": ("C1", 48, 64, None, 4),
     "C2": ("C2", 48, 64, None, 2),
+    "C3": ("C3", 48, 64, None, 1),  # the bench config itself (first GN iteration)
     "C4": ("C4", 48, 64, None, 2),
-    "C5": ("C5", 24, 32, 40, 3),
+    "C5": ("C5", 48, 64, None, 2),
 }
 
 
