@@ -48,14 +48,14 @@ struct EnergyArgs {
   double* part;  // (NL * tiles) per-CTA energies
 };
 
-// flow records of the thread's pixel are staged in shared memory (cp.async, one
-// burst per CTA) when the frame's out-degree allows (else both walks read through L1)
-constexpr int kEnergyStageMax = 16;  // without staging: 72 us vs 66 us on C3
+// flow records of the thread's pixel are staged in shared memory (cp.async, one burst
+// per CTA; reading them through L1 in both walks measured 72 us vs 66 us on C3); the
+// compiled out-degree limit keeps the stage within 64 KB
+static_assert(kMaxOutDegree <= 16, "energy_kernel stages kMaxOutDegree x 256 flow records");
 
 __host__ __device__ inline size_t energy_smem_bytes(int kmax) {
   const size_t k = (size_t)(kmax > 0 ? kmax : 1);
-  const size_t stage = kmax <= kEnergyStageMax ? sizeof(float4) * kEnergyTile * k : 0;
-  return stage + (sizeof(EdgeLin) + sizeof(EdgeBack) + sizeof(float4*)) * k;
+  return (sizeof(float4) * kEnergyTile + sizeof(EdgeLin) + sizeof(EdgeBack) + sizeof(float4*)) * k;
 }
 
 // pix_terms with the hardware reciprocal (rcp.approx, <= 1 ulp): the energy walk
@@ -92,9 +92,8 @@ __global__ void __launch_bounds__(kEnergyThreads) energy_kernel(const EnergyArgs
   const int fl = blockIdx.x / A.tiles, tile = blockIdx.x % A.tiles;
   const int s0 = A.csr_off[fl], k = A.csr_off[fl + 1] - s0;
   const int f = A.frame_of[fl];
-  const bool stage = A.kmax <= kEnergyStageMax;
-  float4* fs = reinterpret_cast<float4*>(smem);  // [k][256] when staged
-  EdgeLin* sl = reinterpret_cast<EdgeLin*>(smem + (stage ? sizeof(float4) * kEnergyTile * A.kmax : 0));
+  float4* fs = reinterpret_cast<float4*>(smem);  // [kmax][256]
+  EdgeLin* sl = reinterpret_cast<EdgeLin*>(smem + sizeof(float4) * kEnergyTile * A.kmax);
   EdgeBack* sb = reinterpret_cast<EdgeBack*>(sl + k);
   const float4** fp0 = reinterpret_cast<const float4**>(sb + k);
   const int tid = threadIdx.x;
@@ -121,7 +120,7 @@ __global__ void __launch_bounds__(kEnergyThreads) energy_kernel(const EnergyArgs
 
   // the thread's pixels p_j = tile*256 + j*kEnergyThreads + tid, each with its k flow
   // records staged in shared memory in one burst (each thread reads back only its own,
-  // so no barrier); without staging both walks read through L1
+  // so no barrier)
   bool in[kEnergyPx];
   int pc[kEnergyPx];
 #pragma unroll
@@ -130,19 +129,14 @@ __global__ void __launch_bounds__(kEnergyThreads) energy_kernel(const EnergyArgs
     in[j] = p < P;
     pc[j] = in[j] ? p : 0;  // clamped: out-of-range pixels read pixel 0 and contribute nothing
   }
-  if (stage) {
-    for (int a = 0; a < k; ++a)
+  for (int a = 0; a < k; ++a)
 #pragma unroll
-      for (int j = 0; j < kEnergyPx; ++j) {
-        const unsigned dst =
-            (unsigned)__cvta_generic_to_shared(fs + a * kEnergyTile + j * kEnergyThreads + tid);
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(fp0[a] + pc[j]));
-      }
-    asm volatile("cp.async.commit_group;");
-  }
-  auto record = [&](int a, int j) -> float4 {
-    return stage ? fs[a * kEnergyTile + j * kEnergyThreads + tid] : __ldg(fp0[a] + pc[j]);
-  };
+    for (int j = 0; j < kEnergyPx; ++j) {
+      const unsigned dst = (unsigned)__cvta_generic_to_shared(fs + a * kEnergyTile + j * kEnergyThreads + tid);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(fp0[a] + pc[j]));
+    }
+  asm volatile("cp.async.commit_group;");
+  auto record = [&](int a, int j) -> float4 { return fs[a * kEnergyTile + j * kEnergyThreads + tid]; };
   const float Wf = (float)A.W, Hf = (float)A.H;
   const float fxn = (float)A.intr_n[0], fyn = (float)A.intr_n[1];
   const float cxn = (float)A.intr_n[2], cyn = (float)A.intr_n[3];
@@ -156,7 +150,7 @@ __global__ void __launch_bounds__(kEnergyThreads) energy_kernel(const EnergyArgs
     dn[j] = dc[j];
     ap[j] = A.prior != nullptr ? A.alpha * (A.pweight ? A.pweight[f] : 1.f) * (float)A.pmask[fpx] : 0.f;
   }
-  if (stage) asm volatile("cp.async.wait_all;" ::: "memory");
+  asm volatile("cp.async.wait_all;" ::: "memory");
   if (phaseA) {
     const float fxc = (float)A.intr_c[0], fyc = (float)A.intr_c[1];
     const float cxc = (float)A.intr_c[2], cyc = (float)A.intr_c[3];

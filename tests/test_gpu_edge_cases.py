@@ -81,3 +81,4 @@ def test_every_pose_fixed(torch_cuda):
     fixed = np.ones(len(wl.frames), dtype=bool)
     P, _, _ = _check(wl, 2, fixed=fixed)
     assert np.array_equal(P, wl.poses0)
+
