@@ -904,7 +904,7 @@ int launch_prep(Ctx& c, int cur, int nxt, bool init, int cand = 0) {
 
 template <bool CALIB>
 int launch_pass_t(Ctx& c, const PassArgs& a) {
-  auto k = a.stage ? pass_kernel<CALIB, true> : pass_kernel<CALIB, false>;
+  auto k = pass_kernel<CALIB>;
   DBA_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.p->pass_smem));
   auto& pr = c.p->prof;
   std::pair<int, int> ev{-1, -1};

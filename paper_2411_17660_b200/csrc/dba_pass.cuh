@@ -186,15 +186,14 @@ __device__ __forceinline__ PixTerms pix_terms(const float R[9], const float t[3]
   return o;
 }
 
-// STAGE mirrors A.stage as a template argument: no per-record staged/L1 select in the walks
-template <bool CALIB, bool STAGE>
+template <bool CALIB>
 __global__ void __launch_bounds__(kPassThreads, 1) pass_kernel(const PassArgs A) {
   pdl_enter();
   if (trial_skipped(A.status)) return;
   if (A.runs && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(A.runs, 1ull);
   extern __shared__ __align__(16) unsigned char smem[];
   constexpr int NVE = kEdgeVals + (CALIB ? kCalibVals : 0);
-  const PassSmem L = pass_smem_layout(A.kmax, CALIB, STAGE);
+  const PassSmem L = pass_smem_layout(A.kmax, CALIB, A.stage != 0);
   float4* fbuf = reinterpret_cast<float4*>(smem + L.fbuf);  // [k][kSub] flow records
   float* U = reinterpret_cast<float*>(smem + L.U);
   float* Mg = reinterpret_cast<float*>(smem + L.U);  // segment end only: [32][kPassThreads]
@@ -318,14 +317,14 @@ __global__ void __launch_bounds__(kPassThreads, 1) pass_kernel(const PassArgs A)
       }
       asm volatile("cp.async.commit_group;");
     };
-    if (STAGE) prefetch(A.seg_t0[sg]);
+    if (A.stage) prefetch(A.seg_t0[sg]);
 
     for (int tile = A.seg_t0[sg]; tile < A.seg_t1[sg]; ++tile) {
       const int pbase = tile * kSub;
-      if (STAGE) asm volatile("cp.async.wait_all;" ::: "memory");
+      if (A.stage) asm volatile("cp.async.wait_all;" ::: "memory");
       if (tid < kSub) {
         const int p = pbase + tid;
-        if (!STAGE) dcs[tid] = p < P ? A.d_cur[(size_t)f * P + p] : 0.f;
+        if (!A.stage) dcs[tid] = p < P ? A.d_cur[(size_t)f * P + p] : 0.f;
         const float pu = (float)(p % A.W), pv = (float)(p / A.W);
         qcs[tid] = make_float2((pu - cxc) / fxc, (pv - cyc) / fyc);
         qns[tid] = make_float2((pu - cxn) / fxn, (pv - cyn) / fyn);
@@ -344,7 +343,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) pass_kernel(const PassArgs A)
 #ifndef DBA_PASS_SKIP_A
         for (int a = eg; a < k; a += 2) {
           const EdgeBack& e = sb[a];
-          const float4 fw = STAGE ? fbuf[a * kSub + pl]
+          const float4 fw = A.stage ? fbuf[a * kSub + pl]
                                     : (in ? __ldg(A.flow + (size_t)sflow[a] * P + p) : make_float4(0.f, 0.f, 0.f, 0.f));
           const PixTerms T = pix_terms(e.R, e.t, qx, qy, dc, fxc, fyc, cxc, cyc, Wf, Hf, fw, in);
           const float fxi = fxc * T.iz, fyi = fyc * T.iz;
@@ -416,7 +415,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) pass_kernel(const PassArgs A)
         {
           const int pl = sl0 + lane, p = pbase + pl;
           const bool in = p < P;
-          const float4 fw = STAGE ? fbuf[a * kSub + pl]
+          const float4 fw = A.stage ? fbuf[a * kSub + pl]
                                     : (in ? __ldg(fl4 + p) : make_float4(0.f, 0.f, 0.f, 0.f));
           const float dn = dns[pl];
           const float2 q = qns[pl];
@@ -523,7 +522,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) pass_kernel(const PassArgs A)
         }
       }
       __syncthreads();
-      if (STAGE && tile + 1 < A.seg_t1[sg]) prefetch(tile + 1);  // overlaps the GEMM
+      if (A.stage && tile + 1 < A.seg_t1[sg]) prefetch(tile + 1);  // overlaps the GEMM
       // ------------------------------------------------------------ per pixel
       // two threads per pixel: both form C_p, g_d,p; each scales half of the row
       {
