@@ -425,6 +425,8 @@ def main():
         Kh = torch.as_tensor(inp["intr0"]).pin_memory()
         e2e_ms = 0.0
         e2e_trials = 0
+        Pc = torch.empty(Ph.shape, dtype=torch.float64).pin_memory()
+        Dc = torch.empty(Dh.shape, dtype=torch.float32).pin_memory()
         for step in range(args.steps + 1):
             flush.zero_()
             barrier()
@@ -433,7 +435,8 @@ def main():
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(st)
             Po, Do, Ko, rep = solver.solve(Ph, Dh, Kh, Fh, iters=args.iters)
-            Pc, Dc = Po.cpu(), Do.cpu()
+            Pc.copy_(Po, non_blocking=True)  # results read back into pinned host buffers
+            Dc.copy_(Do, non_blocking=True)
             e1.record(st)
             torch.cuda.synchronize()
             barrier()
