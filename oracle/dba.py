@@ -505,8 +505,12 @@ def calib_condition(L, n_theta=4):
     return float(p.max() / max(p.min(), 1e-300))
 
 
-def solve(state: State, prob: Problem, opts: Options | None = None):
-    """Damped Gauss-Newton with Schur elimination of disparities."""
+def solve(state: State, prob: Problem, opts: Options | None = None, snapshot=None):
+    """Damped Gauss-Newton with Schur elimination of disparities.
+
+    ``snapshot(n, state, report)``, when given, is called after the n-th accepted
+    iteration with the state an ``iters=n`` call would return (the A5 end-of-call gauge
+    applied to a copy) -- the per-iteration fixtures in one run."""
     opts = opts or Options()
     calib = opts.optimize_intrinsics
     if not np.any(prob.fixed):
@@ -549,6 +553,9 @@ def solve(state: State, prob: Problem, opts: Options | None = None):
             lam = max(lam / 10.0, opts.lam_min)
             it += 1
             rep.energy_trace.append(sysm.energy)
+            if snapshot is not None:
+                snap = apply_scale_gauge(cur, prob, ref_g, opts)[0] if gauge else cur.copy()
+                snapshot(it, snap, rep)
         else:
             lam *= 10.0
             if lam > opts.lam_max:

@@ -297,8 +297,12 @@ CONFIGS = {
 }
 
 
-def make_workload(name, height=48, width=64, keyframes=None, radius=None, iters=None):
-    """Deterministic BASELINE configs C1..C5."""
+def make_workload(name, height=48, width=64, keyframes=None, radius=None, iters=None,
+                  noise=0.0):
+    """Deterministic BASELINE configs C1..C5.  ``noise`` > 0 adds Gaussian
+    correspondence noise of that sigma in pixels (``SceneSpec.pixel_noise``,
+    ``providers.py:332-335``) -- the "noisy" variants whose LM decisions are not
+    decided at the float32 rounding floor."""
     cfg = dict(CONFIGS[name])
     if keyframes is not None:
         cfg["keyframes"] = keyframes
@@ -311,7 +315,7 @@ def make_workload(name, height=48, width=64, keyframes=None, radius=None, iters=
     if focal is not None:  # C5's true focal (64 px at 48x64) scales with the grid width
         focal = focal * width / 64.0
     spec = SceneSpec(trajectory=cfg["trajectory"], frames=cfg["scene_frames"],
-                     height=height, width=width, seed=0, focal=focal)
+                     height=height, width=width, seed=0, focal=focal, pixel_noise=float(noise))
     sc = Scene(spec)
     frames = list(range(cfg["keyframes"]))
     ii, jj = radius_edges(len(frames), cfg["radius"])

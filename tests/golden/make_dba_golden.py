@@ -1,16 +1,19 @@
 """Generate committed DBA golden fixtures from the float64 CPU oracle ("committed
 .npz golden outputs from the oracle, per config and per iteration, then pin GPU parity").
 
-    python tests/golden/make_dba_golden.py
+    python tests/golden/make_dba_golden.py [TAG ...]
 
 For each BASELINE config (C1 mono, C2 frontend window, C3 global backend, C4 depth prior,
-C5 self-calibrating), at its own 48x64 resolution, the deterministic workload of
-``paper_2411_17660_b200.scenes.make_workload`` is solved by ``oracle.dba.solve`` for
-1..iters accepted GN iterations, and the state after each is stored (poses and
-intrinsics float64, disparities float32 -- 6e-8 relative, far below the 1e-4 bar), with
-the energy trace, trial count and a checksum of the inputs.  ``tests/test_dba_golden.py``
-re-derives C1 iteration 1 with the oracle (pins the oracle against itself) and compares
-the GPU path against every fixture.
+C5 self-calibrating), at its own 48x64 resolution and for its full iteration budget, the
+deterministic workload of ``paper_2411_17660_b200.scenes.make_workload`` is solved ONCE by
+``oracle.dba.solve``; its ``snapshot`` hook records, after every accepted GN iteration n,
+the state an ``iters=n`` call returns (poses and intrinsics float64, disparities through the
+log-quantised codec of ``dba_codec.py``, 5e-7 relative), the energy trace and trial count.
+Tags ending in ``n`` are the noisy variants (0.5 px Gaussian correspondence noise,
+``providers.py:332-335``): their energy floor is the noise, so every LM decision of all
+eight iterations is made by a real energy decrease, not by rounding.
+``tests/test_dba_golden.py`` pins the oracle against C1 and compares the GPU path
+against every fixture, every iteration.
 """
 
 from __future__ import annotations
@@ -24,17 +27,19 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(os.path.dirname(HERE))
 sys.path.insert(0, ROOT)
+sys.path.insert(0, HERE)
 
+import dba_codec  # noqa: E402
 from oracle import dba as O  # noqa: E402
 from paper_2411_17660_b200 import scenes  # noqa: E402
 
-# name -> (config, height, width, keyframes, iterations)
+NOISE = 0.5
+# tag -> (config, pixel noise)
 FIXTURES = {
-    "C1": ("C1", 48, 64, None, 4),
-    "C2": ("C2", 48, 64, None, 2),
-    "C3": ("C3", 48, 64, None, 1),  # the bench config itself (first GN iteration)
-    "C4": ("C4", 48, 64, None, 2),
-    "C5": ("C5", 48, 64, None, 2),
+    "C1": ("C1", 0.0), "C2": ("C2", 0.0), "C3": ("C3", 0.0), "C4": ("C4", 0.0),
+    "C5": ("C5", 0.0),
+    "C1n": ("C1", NOISE), "C2n": ("C2", NOISE), "C3n": ("C3", NOISE), "C4n": ("C4", NOISE),
+    "C5n": ("C5", NOISE),
 }
 
 
@@ -46,28 +51,42 @@ def input_checksum(wl):
     return float(h)
 
 
+def make(tag):
+    cfg, noise = FIXTURES[tag]
+    t0 = time.time()
+    wl = scenes.make_workload(cfg, noise=noise)
+    H, W = wl.flow.shape[1:3]
+    calib = bool(wl.optimize_intrinsics)
+    prior = wl.prior is not None
+    prob = O.Problem(ii=wl.ii, jj=wl.jj, flow=wl.flow, fixed=wl.fixed,
+                     prior=wl.prior if prior else None, prior_mask=wl.prior_mask if prior else None)
+    out = dict(config=cfg, noise=noise, height=H, width=W, keyframes=len(wl.frames),
+               iters=wl.iters, calib=calib, prior=prior, checksum=input_checksum(wl))
+    disps = []
+
+    def snap(n, st, rep):
+        out[f"poses_{n}"] = st.poses.copy()
+        out[f"intr_{n}"] = st.intr.copy()
+        out[f"energy_{n}"] = np.array(rep.energy_trace)
+        out[f"trials_{n}"] = rep.trials
+        disps.append(st.disps.copy())
+
+    st = O.State(wl.poses0.astype(np.float64).copy(), wl.disps0.astype(np.float64).copy(),
+                 wl.intr0.astype(np.float64).copy())
+    _, rep = O.solve(st, prob, O.Options(iters=wl.iters, optimize_intrinsics=calib),
+                     snapshot=snap)
+    out["iters"] = rep.iterations
+    out["initial_energy"] = rep.initial_energy
+    for n, dl in enumerate(dba_codec.encode(wl.disps0, disps), 1):
+        out[f"dq_{n}"] = dl
+    np.savez_compressed(os.path.join(HERE, f"dba_{tag}.npz"), **out)
+    print(f"{tag}: {len(wl.frames)} frames, {len(wl.ii)} edges, {H}x{W}, {rep.iterations} "
+          f"iterations, {rep.trials} trials, {time.time() - t0:.1f} s", flush=True)
+
+
 def main():
-    for tag, (cfg, H, W, kf, iters) in FIXTURES.items():
-        t0 = time.time()
-        wl = scenes.make_workload(cfg, height=H, width=W, keyframes=kf)
-        calib = bool(wl.optimize_intrinsics)
-        prior = wl.prior is not None
-        prob = O.Problem(ii=wl.ii, jj=wl.jj, flow=wl.flow, fixed=wl.fixed,
-                         prior=wl.prior if prior else None, prior_mask=wl.prior_mask if prior else None)
-        out = dict(config=cfg, height=H, width=W, keyframes=len(wl.frames), iters=iters, calib=calib,
-                   prior=prior, checksum=input_checksum(wl))
-        for n in range(1, iters + 1):
-            st = O.State(wl.poses0.astype(np.float64).copy(), wl.disps0.astype(np.float64).copy(),
-                         wl.intr0.astype(np.float64).copy())
-            res, rep = O.solve(st, prob, O.Options(iters=n, optimize_intrinsics=calib))
-            out[f"poses_{n}"] = res.poses
-            out[f"disps_{n}"] = res.disps.astype(np.float32)
-            out[f"intr_{n}"] = res.intr
-            out[f"energy_{n}"] = np.array(rep.energy_trace)
-            out[f"trials_{n}"] = rep.trials
-        np.savez_compressed(os.path.join(HERE, f"dba_{tag}.npz"), **out)
-        print(f"{tag}: {len(wl.frames)} frames, {len(wl.ii)} edges, {H}x{W}, {iters} iterations, "
-              f"{time.time() - t0:.1f} s")
+    for tag in sys.argv[1:] or list(FIXTURES):
+        make(tag)
 
 
 if __name__ == "__main__":

@@ -1,11 +1,21 @@
 """Committed DBA golden fixtures (tests/golden/dba_*.npz, made by make_dba_golden.py from
 the float64 oracle): the oracle is pinned against them on CPU, the GPU path is compared to
-them per config and per GN iteration (SURVEY §8c/§8d parity bar: 1e-4 relative on every
-disparity and pose translation)."""
+them per config and per GN iteration, for every iteration of each config's budget, on the
+clean workloads and on their noisy variants (tags ``*n``: 0.5 px correspondence noise).
+
+The bar is the north star's, unrelaxed: after EVERY GN iteration,
+  max over all pixels |d - d_ref| / d_ref < 1e-4,
+  max over poses |t - t_ref| / |t_ref| < 1e-4 and rotation within 1e-4 rad-equivalent,
+  intrinsics (C5) relative 1e-4,
+the same accepted-iteration count, and (noisy variants, where every LM decision is made by
+a real energy decrease rather than at the float32 rounding floor) the same trial count and
+energy trace within 1e-4 relative.
+"""
 
 from __future__ import annotations
 
 import os
+import sys
 
 import numpy as np
 import pytest
@@ -14,8 +24,14 @@ from oracle import dba as O
 from paper_2411_17660_b200 import scenes
 
 GOLD = os.path.join(os.path.dirname(__file__), "golden")
-TAGS = ["C1", "C2", "C3", "C4", "C5"]
+sys.path.insert(0, GOLD)
+import dba_codec  # noqa: E402
+
+CLEAN = ["C1", "C2", "C3", "C4", "C5"]
+NOISY = ["C1n", "C2n", "C3n", "C4n", "C5n"]
+TAGS = CLEAN + NOISY
 REL_TOL = 1e-4
+_CACHE = {}
 
 
 def _load(tag):
@@ -23,11 +39,16 @@ def _load(tag):
 
 
 def _workload(g):
-    kf = int(g["keyframes"])
-    cfg = str(g["config"])
-    base = scenes.CONFIGS[cfg]["keyframes"]
-    return scenes.make_workload(cfg, height=int(g["height"]), width=int(g["width"]),
-                                keyframes=None if kf == base else kf)
+    key = (str(g["config"]), float(g["noise"]))
+    if key not in _CACHE:
+        _CACHE[key] = scenes.make_workload(key[0], height=int(g["height"]), width=int(g["width"]),
+                                           noise=key[1])
+    return _CACHE[key]
+
+
+def _disps(g, wl):
+    n = int(g["iters"])
+    return dba_codec.decode(wl.disps0, [g[f"dq_{k}"] for k in range(1, n + 1)])
 
 
 def _checksum(wl):
@@ -38,11 +59,35 @@ def _checksum(wl):
     return float(h)
 
 
+def parity_stats(P, D, K, g, n, d_ref):
+    """Per-iteration parity numbers (also used by bench.py's ``parity`` object)."""
+    from tests.helpers import pose_errors
+    te, ae = pose_errors(np.asarray(P), g[f"poses_{n}"])
+    rel = np.abs(np.asarray(D, np.float64) - d_ref) / d_ref
+    out = dict(iteration=n, disp_max=float(rel.max()), disp_p999=float(np.quantile(rel, 0.999)),
+               pose_t=te, pose_deg=ae)
+    if K is not None:
+        out["intr"] = float(np.max(np.abs(np.asarray(K) - g[f"intr_{n}"]) / g[f"intr_{n}"]))
+    return out
+
+
 @pytest.mark.parametrize("tag", TAGS)
 def test_fixture_inputs_match_workload(tag):
     g = _load(tag)
     wl = _workload(g)
     assert _checksum(wl) == float(g["checksum"])
+    assert 1 <= int(g["iters"]) <= wl.iters
+
+
+def test_codec_roundtrip():
+    rng = np.random.default_rng(3)
+    d0 = rng.uniform(1e-3, 2.0, size=(3, 4, 5))
+    ds = [d0 * (1 + 0.05 * rng.normal(size=d0.shape)), None]
+    ds[1] = ds[0] * (1 + 1e-5 * rng.normal(size=d0.shape))
+    ds = [np.maximum(d, 1e-6) for d in ds]
+    back = dba_codec.decode(d0, dba_codec.encode(d0, ds))
+    for a, b in zip(ds, back):
+        assert np.max(np.abs(a - b) / a) <= 0.51 * dba_codec.QUANT * 1.0000001
 
 
 def test_oracle_reproduces_c1_fixture():
@@ -51,10 +96,12 @@ def test_oracle_reproduces_c1_fixture():
     prob = O.Problem(ii=wl.ii, jj=wl.jj, flow=wl.flow, fixed=wl.fixed)
     st = O.State(wl.poses0.astype(np.float64).copy(), wl.disps0.astype(np.float64).copy(),
                  wl.intr0.astype(np.float64).copy())
-    res, rep = O.solve(st, prob, O.Options(iters=1))
-    assert np.allclose(res.poses, g["poses_1"], rtol=1e-12, atol=1e-14)
-    assert np.allclose(res.disps.astype(np.float32), g["disps_1"], rtol=1e-6, atol=0)
-    assert np.allclose(rep.energy_trace, g["energy_1"], rtol=1e-12)
+    ref = _disps(g, wl)
+    res, rep = O.solve(st, prob, O.Options(iters=2))
+    assert np.allclose(res.poses, g["poses_2"], rtol=1e-12, atol=1e-14)
+    assert np.max(np.abs(res.disps - ref[1]) / ref[1]) < 1e-6
+    assert np.allclose(rep.energy_trace, g["energy_2"], rtol=1e-12)
+    assert rep.trials == int(g["trials_2"])
 
 
 @pytest.mark.gpu
@@ -62,33 +109,34 @@ def test_oracle_reproduces_c1_fixture():
 def test_gpu_matches_fixture_per_iteration(tag):
     import torch
     from paper_2411_17660_b200 import dba
-    from tests.helpers import pose_errors
     if not torch.cuda.is_available():
         pytest.fail("GPU tests require a CUDA device")
     g = _load(tag)
     wl = _workload(g)
     calib, prior = bool(g["calib"]), bool(g["prior"])
+    noisy = float(g["noise"]) > 0
     H, W = int(g["height"]), int(g["width"])
-    s = dba.DBASolver(wl.ii, wl.jj, len(wl.frames), H, W, wl.fixed, optimize_intrinsics=calib, use_prior=prior)
+    refs = _disps(g, wl)
+    s = dba.DBASolver(wl.ii, wl.jj, len(wl.frames), H, W, wl.fixed, optimize_intrinsics=calib,
+                      use_prior=prior)
     kw = dict(prior=wl.prior, prior_mask=wl.prior_mask) if prior else {}
+    e0 = float(g["initial_energy"])
+    fails = []
     for n in range(1, int(g["iters"]) + 1):
         Po, Do, Ko, rep = s.solve(wl.poses0, wl.disps0, wl.intr0, wl.flow, iters=n, **kw)
-        assert rep.iterations_run == len(g[f"energy_{n}"])
-        te, ae = pose_errors(Po.cpu().numpy(), g[f"poses_{n}"])
-        assert te < REL_TOL, (tag, n, te)
-        assert ae < 1e-3, (tag, n, ae)
-        d, dr = Do.cpu().numpy().astype(np.float64), g[f"disps_{n}"].astype(np.float64)
-        dprev = (wl.disps0 if n == 1 else g[f"disps_{n - 1}"]).astype(np.float64)
-        # relative to the state magnitude max(d_ref, d_prev), as in test_gpu_parity: pixels a
-        # step drives towards zero disparity carry the step's absolute error
-        rel = np.abs(d - dr) / np.maximum(dr, dprev)
-        assert np.quantile(rel, 0.9999) < REL_TOL, (tag, n, np.quantile(rel, 0.9999))
-        # C3 (300-frame chain): the back-substitution of a few pixels cancels gradient and
-        # pose-step terms almost exactly, amplifying the 1e-5-level pose-step differences of
-        # the chain's weak bending modes (1 pixel of 921,600 at 4.5e-4 in iteration 1)
-        bad = int(np.count_nonzero(rel >= REL_TOL))
-        assert bad <= 1e-5 * rel.size and rel.max() < 1e-3, (tag, n, bad, rel.max())
-        if calib:
-            assert np.max(np.abs(Ko.cpu().numpy() - g[f"intr_{n}"]) / g[f"intr_{n}"]) < REL_TOL
-        e_ref = g[f"energy_{n}"][-1]
-        assert abs(rep.final_energy - e_ref) <= REL_TOL * rep.initial_energy
+        st = parity_stats(Po.cpu().numpy(), Do.cpu().numpy(), Ko.cpu().numpy() if calib else None,
+                          g, n, refs[n - 1])
+        print(tag, st, "trials", rep.trials, int(g[f"trials_{n}"]))
+        ok = (rep.iterations_run == n and st["disp_max"] < REL_TOL and st["pose_t"] < REL_TOL
+              and st["pose_deg"] < np.degrees(REL_TOL) and st.get("intr", 0.0) < REL_TOL)
+        tr, tr_ref = np.array(rep.energy_trace), g[f"energy_{n}"]
+        if noisy:
+            ok = ok and rep.trials == int(g[f"trials_{n}"])
+            ok = ok and np.all(np.abs(tr - tr_ref) <= REL_TOL * tr_ref)
+        else:
+            # clean data ends at the float32 rounding floor of the residuals (~1e-11 of the
+            # initial energy), far below which the oracle keeps converging in float64
+            ok = ok and np.all(np.abs(tr - tr_ref) <= REL_TOL * tr_ref + 1e-11 * e0)
+        if not ok:
+            fails.append((n, st, rep.trials, int(g[f"trials_{n}"])))
+    assert not fails, fails
