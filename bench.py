@@ -17,8 +17,11 @@ e2e     = the same metric through the public tensor API from pinned HOST buffers
 roofline= the fused pass kernel (dominant kernel): algorithmic bytes per launch
           (16 B flow record per edge-pixel + 8 B disparity read+write per
           frame-pixel) / its live CUDA-event launch duration, vs MEASURED_PEAKS
-cpu_baseline = the float64 numpy oracle (oracle/dba.py, "port") on a bounded
-          sample of the same workload on this host's cores.
+cpu_baseline = the float64 numpy oracle (oracle/dba.py, "port") on this host's cores:
+          complete GN iterations over the FULL C3 graph (median of 3 after a warm-up);
+          --impl reference times the same, one full-graph GN iteration per step, and
+          never loads the CUDA library.
+--gpus N outside torchrun re-launches itself as N local ranks (torch.distributed.run).
 """
 
 from __future__ import annotations
@@ -39,6 +42,12 @@ if ROOT not in sys.path:
 CONFIG = "C3"
 H, W = 48, 64
 FALLBACK_HBM_GBS = 6650.0
+THREAD_VARS = ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS")
+# the CPU legs use every host core the process may run on (BASELINE.md CPU-baseline plan);
+# pinned before numpy is imported
+for _v in THREAD_VARS:
+    os.environ.setdefault(_v, str(len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity")
+                                  else os.cpu_count()))
 
 
 def parse():
@@ -202,19 +211,24 @@ def compute_roofline(inp, H, W, pass_ms):
             "peak_kind": "nominal fp32 FMA (measured FFMA microbenchmark: 122-127 FFMA/clk/SM)"}
 
 
-def build_inputs(keyframes, rank, nranks):
-    """Scene, graph and THIS rank's flow rows (local edges in input order)."""
+def build_inputs(keyframes, rank, nranks, partition=None):
+    """Scene, graph and THIS rank's flow rows (local edges in input order).  ``partition``
+    is the frame partition function (the library's ``dba.partition`` on the GPU arm; the
+    reference arm never loads the library and runs the whole graph on one rank)."""
     import numpy as np
 
-    from paper_2411_17660_b200 import dba, scenes
+    from paper_2411_17660_b200 import scenes
     cfg = scenes.CONFIGS[CONFIG]
     spec = scenes.SceneSpec(trajectory=cfg["trajectory"], frames=max(cfg["scene_frames"], keyframes),
                             height=H, width=W, seed=0)
     sc = scenes.Scene(spec)
     frames = list(range(keyframes))
     ii, jj = scenes.radius_edges(keyframes, cfg["radius"])
-    bounds = dba.partition(ii, keyframes, nranks)
-    f0, f1 = int(bounds[rank]), int(bounds[rank + 1])
+    if nranks == 1:
+        f0, f1 = 0, keyframes
+    else:
+        bounds = partition(ii, keyframes, nranks)
+        f0, f1 = int(bounds[rank]), int(bounds[rank + 1])
     local = [e for e in range(len(ii)) if f0 <= ii[e] < f1]
     flow = np.stack([sc.flow_record(int(ii[e]), int(jj[e])) for e in local]) if local else \
         np.zeros((0, H, W, 4), np.float32)
@@ -225,57 +239,102 @@ def build_inputs(keyframes, rank, nranks):
                 intr0=sc.intr.copy(), fixed=fixed, f0=f0, f1=f1, local=local)
 
 
-def cpu_baseline(steps=1, sample_frames=24):
-    """float64 oracle (oracle/dba.py) on a bounded sample: one GN trial on the C3
-    sub-graph of keyframes 0..sample_frames-1 (same scene, resolution, radius)."""
-    import numpy as np
+def host_cores():
+    return len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
 
-    from oracle import dba as O
-    inp = build_inputs(sample_frames, 0, 1)
-    prob = O.Problem(inp["ii"], inp["jj"], inp["flow"], inp["fixed"])
-    st = O.State(inp["poses0"].copy(), inp["disps0"].astype(np.float64), inp["intr0"].copy())
-    opts = O.Options()
-    sysm = O.linearize(st, prob, opts)
-    times = []
-    for _ in range(steps):
+
+def blas_threads():
+    """The thread counts the CPU arm actually runs with (pinned at the top of bench.py)."""
+    out = {k: os.environ.get(k) for k in THREAD_VARS}
+    try:
+        from threadpoolctl import threadpool_info
+        out["threadpools"] = [{"api": d.get("internal_api"), "threads": d.get("num_threads")}
+                              for d in threadpool_info()]
+    except Exception:
+        pass
+    return out
+
+
+class CpuGN:
+    """The reference CPU path on the FULL bench workload: one complete damped-GN iteration
+    of the float64 oracle (``oracle/dba.py``; reduced system -> Cholesky -> back-substitute
+    + retract -> relinearise at the trial state, which also yields the trial energy) over
+    all E edges of the C3 graph, timed per iteration.  The linearisation of the starting
+    state is built once outside the timed region; every timed iteration starts from it."""
+
+    def __init__(self, keyframes):
+        import numpy as np
+
+        from oracle import dba as O
+        self.O = O
+        self.inp = build_inputs(keyframes, 0, 1)
+        inp = self.inp
+        self.prob = O.Problem(inp["ii"], inp["jj"], inp["flow"], inp["fixed"])
+        self.st = O.State(inp["poses0"].copy(), inp["disps0"].astype(np.float64), inp["intr0"].copy())
+        self.opts = O.Options()
+        self.sysm = O.linearize(self.st, self.prob, self.opts)
+        self.edges = len(inp["ii"])
+
+    def iteration(self):
+        O = self.O
         t0 = time.perf_counter()
-        Sr, yr, _ = O.reduced(sysm, prob, opts)
-        delta, _ = O.solve_reduced(Sr, yr, opts.lam0)
-        dxi, dth = O.split_step(delta, prob.fixed, False)
-        dxi = O.clamp_tangents(dxi, opts.tangent_max)
-        trial = O.backsub_and_retract(st, prob, opts, dxi, dth)
-        O.linearize(trial, prob, opts)
-        times.append(time.perf_counter() - t0)
-    E = len(inp["ii"])
+        Sr, yr, _ = O.reduced(self.sysm, self.prob, self.opts)
+        delta, _ = O.solve_reduced(Sr, yr, self.opts.lam0)
+        dxi, dth = O.split_step(delta, self.prob.fixed, False)
+        dxi = O.clamp_tangents(dxi, self.opts.tangent_max)
+        trial = O.backsub_and_retract(self.st, self.prob, self.opts, dxi, dth)
+        tsys = O.linearize(trial, self.prob, self.opts)
+        assert tsys.energy <= self.sysm.energy  # an accepted iteration, like the GPU's count
+        return time.perf_counter() - t0
+
+    def describe(self, n, t):
+        return (f"{n} complete GN iteration(s) (reduced solve + Cholesky + back-substitution + "
+                f"retraction + relinearisation) of the float64 oracle over the FULL {CONFIG} graph "
+                f"({self.edges} edges, {H}x{W}), median {t:.2f} s per iteration")
+
+
+def cpu_baseline(keyframes, samples=3):
+    """GPU arm's reported CPU baseline: median of ``samples`` full-graph GN iterations
+    after one untimed warm-up iteration (BASELINE.md "CPU-baseline plan")."""
+    g = CpuGN(keyframes)
+    g.iteration()
+    times = [g.iteration() for _ in range(samples)]
     t = statistics.median(times)
-    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
-    return {"value": E * H * W / t, "unit": "edge-px/s", "cores": cores, "kind": "port",
-            "sample": f"1 GN trial (solve+back-substitute+relinearise) on the C3 sub-graph of "
-                      f"keyframes 0..{sample_frames - 1} ({E} edges, {H}x{W}), float64 numpy, "
-                      f"median of {steps}, {t:.2f} s each"}
+    P = H * W
+    return {"value": g.edges * P / t, "unit": "edge-px/s", "cores": host_cores(), "kind": "port",
+            "ms_per_gn_iter": t * 1e3, "threads": blas_threads(),
+            "sample": g.describe(samples, t) + f", after 1 warm-up iteration"}
 
 
 def run_reference(args):
+    """--impl reference: the reference CPU path (float64 oracle restating SPEC.md:286-394; the
+    reference ships no dba module) on the host cores, one full-graph GN iteration per step.
+    Never loads libdba_b200 or CUDA."""
     rank, _, world = dist_env()
     if rank != 0:
         return
-    steps = []
+    g = CpuGN(args.keyframes)
     for _ in range(args.warmup):
-        cpu_baseline(1, sample_frames=24)
-    for _ in range(args.steps):
-        steps.append(cpu_baseline(1, sample_frames=24))
-    v = statistics.median(s["value"] for s in steps)
-    cb = dict(steps[-1])
-    cb["value"] = v
+        g.iteration()
+    times = [g.iteration() for _ in range(args.steps)]
+    P = H * W
+    total = sum(times)
+    v = g.edges * P * len(times) / total
+    t_med = statistics.median(times)
+    cb = {"value": v, "unit": "edge-px/s", "cores": host_cores(), "kind": "port",
+          "threads": blas_threads(), "ms_per_gn_iter": total / len(times) * 1e3,
+          "sample": g.describe(len(times), t_med) + f", {args.warmup} warm-up iteration(s)"}
     out = {
         "impl": "reference", "metric": "dba_gn_edge_pixels_per_sec", "value": v,
         "unit": "edge-px/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": total / len(times) * 1e3, "ms_per_gn_iter": total / len(times) * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": config_dict(args, world),
+        "data": "synthetic",
+        "config": dict(config_dict(args, 1), step="one accepted GN iteration of the full graph"),
         "cpu_baseline": cb,
         "e2e": {"value": v, "unit": "edge-px/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "note": "reference CPU path = float64 numpy restatement of SPEC.md:286-394 (the "
-                "reference ships no dba module); bounded sample per step",
+                "reference ships no dba module); each step is one GN iteration over all edges",
     }
     print(json.dumps(out))
 
@@ -289,8 +348,26 @@ def config_dict(args, world):
             "l2": "flushed between steps (512 MiB write); flow record 146 MB > L2 126 MB"}
 
 
+def spawn_ranks(args):
+    """``python bench.py --gpus N`` outside torchrun: re-launch this script as N local ranks
+    (one process per GPU, 127.0.0.1 rendezvous) and return their exit status."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")  # communicator init lines (nranks) on stdout
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd, env=env)
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args))
     if args.impl == "reference":
         run_reference(args)
         return
@@ -305,7 +382,7 @@ def main():
     dev = torch.device("cuda", local_rank)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    inp = build_inputs(args.keyframes, rank, world)
+    inp = build_inputs(args.keyframes, rank, world, dba.partition)
     N = args.keyframes
     comm = None
     if world > 1:
@@ -455,7 +532,7 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        cpu = cpu_baseline(1, sample_frames=24)
+        cpu = cpu_baseline(args.keyframes)
 
     if rank == 0:
         ms_step = total_ms / args.steps

@@ -99,6 +99,10 @@ typedef struct {
   int32_t damping_candidates; /* lambda values factored per round by dba_solve (lambda, 10 lambda,
                                  ...; 0 = default 3, max 3).  A rejection then costs no new
                                  factorisation; results are identical for every value. */
+  int32_t no_refine;    /* 0 (default): every reduced solve takes one step of iterative
+                           refinement (float64 residual from the original band, the stored
+                           factors re-applied) -- the block LDL^T alone is ~50x less accurate
+                           than a Cholesky on ill-conditioned monocular chains; 1: off */
 } dba_options;
 
 typedef struct {

@@ -83,6 +83,13 @@ class Options:
     optimize_intrinsics: bool = False
     alpha: float = 1e-3
     scale_gauge: bool | None = None  # None = auto (one fixed pose and no prior)
+    # reduced-system solver: "cholesky" (LAPACK potrf, the reference path) or "lu" (LAPACK
+    # getrf): an equally valid float64 ordering, used to measure the oracle's own
+    # reproducibility floor on ill-conditioned problems (tests/golden/make_dba_golden.py)
+    solver: str = "cholesky"
+    # "reverse": the frame contributions to S, y and the energy are accumulated in reverse
+    # frame order -- another valid float64 summation order (same use as ``solver``)
+    order: str = "forward"
 
 
 @dataclass
@@ -320,6 +327,8 @@ def linearize(state: State, prob: Problem, opts: Options, frames=None,
     edge_energy = np.zeros(E)
     edge_finite = np.ones(E, dtype=bool)
     frame_list = range(N) if frames is None else frames
+    if opts.order == "reverse":
+        frame_list = list(frame_list)[::-1]
     g_frame = gauge_frame(prob, opts)
     gauge_terms = None
     for i in frame_list:
@@ -412,10 +421,12 @@ def _chol_fast(A):
     return L
 
 
-def solve_reduced(Sr, yr, lam):
+def solve_reduced(Sr, yr, lam, solver="cholesky"):
     import scipy.linalg
     A = Sr + lam * np.eye(Sr.shape[0])
     L = _chol_fast(A)
+    if solver == "lu":
+        return np.linalg.solve(A, yr), L
     z = scipy.linalg.solve_triangular(L, yr, lower=True)
     return scipy.linalg.solve_triangular(L, z, lower=True, trans=1), L
 
@@ -532,7 +543,7 @@ def solve(state: State, prob: Problem, opts: Options | None = None, snapshot=Non
     while it < opts.iters:
         Sr, yr, _ = reduced(sysm, prob, opts)
         try:
-            delta, L = solve_reduced(Sr, yr, lam)
+            delta, L = solve_reduced(Sr, yr, lam, opts.solver)
         except OracleSolverFailure:
             lam *= 10.0
             if lam > opts.lam_max:

@@ -82,6 +82,21 @@ def solve_prgbd_bcd(state: O.State, prob: O.Problem, prior, mask, scale=None, of
     return cur, s, o, trace
 
 
+def two_stage_uncalibrated(state: O.State, prob: O.Problem, prior, mask, opts: O.Options | None = None,
+                           calib_iters=8, cycles=2):
+    """stage 1 = solve_ba_calib with the Eq. 4 prior (fixed regulariser)
+    from the caller's (heuristic) intrinsics; OracleCalibDegenerate propagates (no stage 2);
+    stage 2 = solve_prgbd_bcd with the intrinsics frozen."""
+    opts = opts or O.Options()
+    p1 = O.Problem(prob.ii, prob.jj, prob.flow, prob.fixed, prior=np.asarray(prior, np.float64),
+                   prior_mask=mask)
+    o1 = O.Options(**{**opts.__dict__, "iters": calib_iters, "optimize_intrinsics": True})
+    st1, _ = O.solve(state, p1, o1)
+    o2 = O.Options(**{**opts.__dict__, "optimize_intrinsics": False})
+    st2, s, o, trace = solve_prgbd_bcd(st1, prob, prior, mask, opts=o2, cycles=cycles)
+    return st2, s, o, trace
+
+
 def interpolate(pa, pb, tau):
     """se3_interpolate (geometry.py:181-184): exp(tau log(G_b G_a^-1)) G_a."""
     delta = G.se3_log(G.pose_compose(pb, G.pose_inverse(pa)))

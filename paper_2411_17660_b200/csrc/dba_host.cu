@@ -16,8 +16,11 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <atomic>
 #include <functional>
+#include <mutex>
 #include <new>
+#include <unordered_map>
 #include <set>
 #include <utility>
 #include <vector>
@@ -85,7 +88,7 @@ struct Layout {
   size_t off_F, off_f, units, contrib, meta_end;
   // state
   size_t poses[2], intr[2], disps[2], xi, delta, lin, back, adj;
-  size_t part_edge, part_M, part_w, part_frame, part_energy, Fbuf, sys[2], gstate[2], Lband, rLband, mid, flags, ctl, gauge, total;
+  size_t part_edge, part_M, part_w, part_frame, part_energy, Fbuf, sys[2], sys_part[2], e_part, gstate[2], Lband, rLband, mid, flags, ctl, gauge, total;
 };
 
 }  // namespace
@@ -95,7 +98,7 @@ struct dba_plan {
   int calib = 0, prior = 0, freeze_d = 0, gauge_on = 0, gauge_frame = -1, rank = 0, nranks = 1;
   int scalefix = 0, anchor = -1;  // prior-fixed monocular scale: exact-row step correction
   int f0 = 0, f1 = 0, NL = 0, EL = 0, kmax = 0, nb = 0, BW = 0, n_red = 0;
-  int n_tiles = 0, G = 0, nseg = 0, n_units = 0, nve = kEdgeVals, stage = 1;
+  int n_tiles = 0, G = 0, nseg = 0, n_units = 0, nve = kEdgeVals, sub = 128, mb = 6;
   size_t pass_smem = 0, solve_smem = 0;
   long long sys_len = 0;  // doubles in one packed reduced system
   long long spec_delta = 0, spec_Lband = 0, spec_rLband = 0, spec_mid = 0;  // per damping candidate
@@ -122,7 +125,7 @@ struct dba_plan {
   unsigned char* meta_pinned = nullptr;
   Readback* rb = nullptr;
   Control* ctl_h = nullptr;  // pinned mirror of the device GN controller
-  const void* uploaded_ws = nullptr;
+  unsigned long long id = 0;  // process-unique (workspace ownership registry)
   int device = -1;
   // live kernel timing (dba_plan_set_profiling) and launch accounting
   struct Prof {
@@ -139,6 +142,22 @@ struct dba_plan {
     std::vector<std::pair<const char*, double>> tl_sum;
   } prof;
 };
+
+namespace {
+// Which plan's metadata each workspace currently holds (process-wide): a workspace that
+// another plan used since this plan's last call is re-uploaded, so plans may share one
+// scratch workspace in any order (A, B, A).
+std::mutex g_ws_mu;
+std::unordered_map<const void*, unsigned long long> g_ws_owner;
+std::atomic<unsigned long long> g_plan_ids{0};
+
+void ws_forget(const dba_plan* p) {
+  std::lock_guard<std::mutex> lk(g_ws_mu);
+  for (auto it = g_ws_owner.begin(); it != g_ws_owner.end();)
+    it = (it->second == p->id) ? g_ws_owner.erase(it) : std::next(it);
+}
+
+}  // namespace
 
 namespace {
 
@@ -228,6 +247,7 @@ int dba_plan_create(const dba_problem_desc* d, dba_plan** out) {
 
   dba_plan* p = new (std::nothrow) dba_plan();
   if (!p) return DBA_ECAPACITY;
+  p->id = ++g_plan_ids;
   p->N = N;
   p->H = d->height;
   p->W = d->width;
@@ -347,21 +367,23 @@ int dba_plan_create(const dba_problem_desc* d, dba_plan** out) {
   }
 
   // ---- pass decomposition: G CTAs over (frame, 256-px tile) work items
-  p->n_tiles = (p->P + kSub - 1) / kSub;
   {
-    PassSmem s = pass_smem_layout(std::max(p->kmax, 1), p->calib, true);
-    p->stage = 1;
-    if (s.total > 225 * 1024) {  // no room to stage the flow records: read them from L2
-      s = pass_smem_layout(std::max(p->kmax, 1), p->calib, false);
-      p->stage = 0;
+    // 128-pixel tiles, 64 when the frame's shared-memory working set would not fit
+    PassSmem s = pass_smem_layout(std::max(p->kmax, 1), p->calib, 128);
+    p->sub = 128;
+    if (s.total > 225 * 1024) {
+      s = pass_smem_layout(std::max(p->kmax, 1), p->calib, 64);
+      p->sub = 64;
     }
     p->pass_smem = s.total;
-    const int ntiles = pass_ntiles(pass_mpad(std::max(p->kmax, 1), p->calib));
-    if (p->pass_smem > 225 * 1024 || ntiles > kPassThreads) {
+    const int mb = pass_mb(pass_mpad(std::max(p->kmax, 1), p->calib));
+    p->mb = mb <= 6 ? 6 : 12;
+    if (p->pass_smem > 225 * 1024 || mb > 12) {
       delete p;
       return DBA_ECAPACITY;
     }
   }
+  p->n_tiles = (p->P + p->sub - 1) / p->sub;
   int dev = 0, sms = 148;
   if (cudaGetDevice(&dev) == cudaSuccess) {
     cudaDeviceProp prop;
@@ -630,11 +652,15 @@ int dba_plan_create(const dba_problem_desc* d, dba_plan** out) {
   for (int s = 0; s < 2; ++s) {
     L.poses[s] = take(sizeof(double) * 7 * N);
     L.intr[s] = take(sizeof(double) * 4);
-    L.disps[s] = take(sizeof(float) * (size_t)N * p->P);
+    L.disps[s] = take(sizeof(double) * (size_t)N * p->P);
     L.sys[s] = take(sizeof(double) * p->sys_len);
+    // with ranks: this rank's partial system, all-reduced OUT OF PLACE into sys[s], so a
+    // gated-off linearisation (gather skipped) re-sums the same partials (idempotent)
+    L.sys_part[s] = take(sizeof(double) * (p->nranks > 1 ? p->sys_len : 0));
     L.gstate[s] = take(sizeof(double) * (6 * kMaxOutDegree + 8));
   }
   L.xi = take(sizeof(double) * 6 * N);
+  L.e_part = take(sizeof(double) * 4);  // per-rank partial energies of slots 0/1 (ranks)
   p->spec_delta = align_doubles(p->n_red + 4);
   L.delta = take(sizeof(double) * p->spec_delta * kMaxSpec);
   L.lin = take(sizeof(EdgeLin) * p->EL);
@@ -685,6 +711,7 @@ int dba_plan_create(const dba_problem_desc* d, dba_plan** out) {
 
 void dba_plan_destroy(dba_plan* p) {
   if (!p) return;
+  ws_forget(p);
   for (cudaEvent_t e : p->prof.pool) cudaEventDestroy(e);
   if (p->meta_pinned) cudaFreeHost(p->meta_pinned);
   if (p->rb) cudaFreeHost(p->rb);
@@ -847,10 +874,14 @@ int prepare(Ctx& c) {
     DBA_CUDA(cudaMallocHost(&p->rb, sizeof(Readback)));
     DBA_CUDA(cudaMallocHost(&p->ctl_h, sizeof(Control)));
   }
-  if (p->uploaded_ws != c.b->workspace) {
-    DBA_CUDA(cudaMemcpyAsync(c.ws, p->meta_pinned, p->meta.size(), cudaMemcpyHostToDevice, c.st));
-    p->uploaded_ws = c.b->workspace;
+  bool upload;
+  {
+    std::lock_guard<std::mutex> lk(g_ws_mu);
+    auto it = g_ws_owner.find(c.b->workspace);
+    upload = it == g_ws_owner.end() || it->second != p->id;
+    g_ws_owner[c.b->workspace] = p->id;
   }
+  if (upload) DBA_CUDA(cudaMemcpyAsync(c.ws, p->meta_pinned, p->meta.size(), cudaMemcpyHostToDevice, c.st));
   return DBA_OK;
 }
 
@@ -902,9 +933,9 @@ int launch_prep(Ctx& c, int cur, int nxt, bool init, int cand = 0) {
   return DBA_OK;
 }
 
-template <bool CALIB>
+template <bool CALIB, int MB>
 int launch_pass_t(Ctx& c, const PassArgs& a) {
-  auto k = pass_kernel<CALIB>;
+  auto k = pass_kernel<CALIB, MB>;
   DBA_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.p->pass_smem));
   auto& pr = c.p->prof;
   std::pair<int, int> ev{-1, -1};
@@ -913,16 +944,12 @@ int launch_pass_t(Ctx& c, const PassArgs& a) {
     DBA_CUDA(cudaEventRecord(pr.pool[ev.first], c.st));
   }
   if (int s = launch(c, k, dim3(c.p->G), dim3(kPassThreads), c.p->pass_smem, false, a)) return s;
-  mark(c, a.system ? "pass" : "pass-E");
-  if (a.system) {
-    pr.pass_launches++;
-    if (!a.runs) pr.pass_runs++;  // gated launches count on the device
-  } else {
-    pr.energy_launches++;
-  }
+  mark(c, "pass");
+  pr.pass_launches++;
+  if (!a.runs) pr.pass_runs++;  // gated launches count on the device
   if (pr.on) {
     DBA_CUDA(cudaEventRecord(pr.pool[ev.second], c.st));
-    (a.system ? pr.pass_ev : pr.energy_ev).push_back(ev);
+    pr.pass_ev.push_back(ev);
   }
   return cuda_status(cudaGetLastError());
 }
@@ -938,9 +965,9 @@ int launch_pass(Ctx& c, int cur, int nxt, bool backsub, bool system, bool gated 
   a.P = p->P;
   a.n_tiles = p->n_tiles;
   a.kmax = std::max(p->kmax, 1);
+  a.sub = p->sub;
   a.backsub = backsub ? 1 : 0;
-  a.system = system ? 1 : 0;
-  a.stage = p->stage;
+  (void)system;
   a.scalefix = p->scalefix;
   a.status = gated ? gate_word(c) : c.at<int>(p->L.flags);
   a.runs = gated ? &c.at<Readback>(p->L.flags)->runs : nullptr;
@@ -954,15 +981,15 @@ int launch_pass(Ctx& c, int cur, int nxt, bool backsub, bool system, bool gated 
   a.lin = c.at<EdgeLin>(p->L.lin);
   a.back = c.at<EdgeBack>(p->L.back);
   a.flow = reinterpret_cast<const float4*>(c.b->flow);
-  a.d_cur = c.at<float>(p->L.disps[cur]);
-  a.d_new = c.at<float>(p->L.disps[nxt]);
+  a.d_cur = c.at<double>(p->L.disps[cur]);
+  a.d_new = c.at<double>(p->L.disps[nxt]);
   a.prior = p->prior ? c.b->prior : nullptr;
   a.pmask = p->prior ? c.b->prior_mask : nullptr;
   a.pweight = p->prior ? c.b->prior_weight : nullptr;
   a.freeze = p->freeze_d;
-  a.alpha = (float)c.o->alpha;
-  a.eta = (float)c.o->eta;
-  a.d_min = (float)c.o->d_min;
+  a.alpha = c.o->alpha;
+  a.eta = c.o->eta;
+  a.d_min = c.o->d_min;
   a.intr_c = c.at<double>(p->L.intr[cur]);
   a.intr_n = c.at<double>(p->L.intr[nxt]);
   a.gauge_frame = p->gauge_on ? p->gauge_frame : -1;
@@ -974,8 +1001,8 @@ int launch_pass(Ctx& c, int cur, int nxt, bool backsub, bool system, bool gated 
   a.seg_off_edge = c.at<long long>(p->L.seg_off_edge);
   a.seg_off_M = c.at<long long>(p->L.seg_off_M);
   a.seg_off_w = c.at<long long>(p->L.seg_off_w);
-  if (p->calib) return launch_pass_t<true>(c, a);
-  return launch_pass_t<false>(c, a);
+  if (p->calib) return p->mb == 6 ? launch_pass_t<true, 6>(c, a) : launch_pass_t<true, 12>(c, a);
+  return p->mb == 6 ? launch_pass_t<false, 6>(c, a) : launch_pass_t<false, 12>(c, a);
 }
 
 // LM controller inputs: the trial (slot 1) energy, the flags word and the options
@@ -1028,14 +1055,14 @@ int launch_epass(Ctx& c, int cur, int nxt, bool backsub, int cand = 0) {
   a.lin = c.at<EdgeLin>(p->L.lin);
   a.back = c.at<EdgeBack>(p->L.back);
   a.flow = reinterpret_cast<const float4*>(c.b->flow);
-  a.d_cur = c.at<float>(p->L.disps[cur]);
-  a.d_new = c.at<float>(p->L.disps[nxt]);
+  a.d_cur = c.at<double>(p->L.disps[cur]);
+  a.d_new = c.at<double>(p->L.disps[nxt]);
   a.prior = p->prior ? c.b->prior : nullptr;
   a.pmask = p->prior ? c.b->prior_mask : nullptr;
   a.pweight = p->prior ? c.b->prior_weight : nullptr;
-  a.alpha = (float)c.o->alpha;
-  a.eta = (float)c.o->eta;
-  a.d_min = (float)c.o->d_min;
+  a.alpha = c.o->alpha;
+  a.eta = c.o->eta;
+  a.d_min = c.o->d_min;
   a.intr_c = c.at<double>(p->L.intr[cur]);
   a.intr_n = c.at<double>(p->L.intr[nxt]);
   a.gauge_frame = p->gauge_on ? p->gauge_frame : -1;
@@ -1077,8 +1104,10 @@ int launch_energy(Ctx& c, int slot, bool decide, int* status, bool from_epass = 
     f.stride = kFrameVals;
     f.part_frame = c.at<double>(p->L.part_frame);
   }
-  f.energy_out = c.at<double>(p->L.sys[slot]) + p->energy_off;
   const bool multi = c.comm && p->nranks > 1;
+  // with ranks the partial energy is all-reduced out of place: a finalize that returns
+  // at entry (trial skipped) leaves the partial, never an already-summed value, in place
+  f.energy_out = multi ? c.at<double>(p->L.e_part) + slot : c.at<double>(p->L.sys[slot]) + p->energy_off;
   if (decide && !multi) {
     if (int s = launch(c, finalize_decide_kernel, dim3(1), dim3(kFinalThreads), 0, false, f, decide_args(c, cand)))
       return s;
@@ -1090,7 +1119,8 @@ int launch_energy(Ctx& c, int slot, bool decide, int* status, bool from_epass = 
   if (multi) {
     if (!nccl().ok) return DBA_ENCCL;
     double* e = c.at<double>(p->L.sys[slot]) + p->energy_off;
-    if (nccl().AllReduce(e, e, 1, ncclDouble, ncclSum, c.comm, c.st) != ncclSuccess) return DBA_ENCCL;
+    if (nccl().AllReduce(c.at<double>(p->L.e_part) + slot, e, 1, ncclDouble, ncclSum, c.comm, c.st) != ncclSuccess)
+      return DBA_ENCCL;
     int* bad = status + 1;
     if (nccl().AllReduce(bad, bad, 1, ncclInt32, ncclMin, c.comm, c.st) != ncclSuccess) return DBA_ENCCL;
   }
@@ -1140,7 +1170,7 @@ int launch_system(Ctx& c, int slot, bool decide = false, bool gated = false) {
     g.units = c.at<GatherUnit>(p->L.units);
     g.contrib = c.at<Contrib>(p->L.contrib);
     g.Fbuf = c.at<double>(p->L.Fbuf);
-    g.sys = c.at<double>(p->L.sys[slot]);
+    g.sys = (c.comm && p->nranks > 1) ? c.at<double>(p->L.sys_part[slot]) : c.at<double>(p->L.sys[slot]);
     const int threads = 256, warps = threads / 32;
     if (int s = launch(c, gather_kernel, dim3((p->n_units + warps - 1) / warps), dim3(threads), 0, false, g)) return s;
     mark(c, "gather");
@@ -1148,7 +1178,8 @@ int launch_system(Ctx& c, int slot, bool decide = false, bool gated = false) {
   if (c.comm && p->nranks > 1) {
     if (!nccl().ok) return DBA_ENCCL;
     double* sy = c.at<double>(p->L.sys[slot]);
-    if (nccl().AllReduce(sy, sy, (size_t)p->energy_off, ncclDouble, ncclSum, c.comm, c.st) != ncclSuccess)
+    const double* part = c.at<double>(p->L.sys_part[slot]);
+    if (nccl().AllReduce(part, sy, (size_t)p->energy_off, ncclDouble, ncclSum, c.comm, c.st) != ncclSuccess)
       return DBA_ENCCL;
   }
   // an accepted trial's energy is already known (energy_kernel)
@@ -1184,6 +1215,7 @@ int launch_solve(Ctx& c, int slot, int nspec = 1) {
   a.block_pose = c.at<int>(p->L.block_pose);
   a.anchor = p->anchor;
   a.nspec = nspec;
+  a.refine = c.o->no_refine ? 0 : 1;
   a.spec_Lband = p->spec_Lband;
   a.spec_rLband = p->spec_rLband;
   a.spec_mid = p->spec_mid;
@@ -1261,11 +1293,11 @@ int initial_pass(Ctx& c) {
                            cudaMemcpyDeviceToDevice, c.st));
   DBA_CUDA(cudaMemcpyAsync(c.at<double>(p->L.intr[0]), c.b->intr_in, sizeof(double) * 4,
                            cudaMemcpyDeviceToDevice, c.st));
-  const size_t fbytes = sizeof(float) * (size_t)p->P;
-  if (p->NL > 0) {
-    DBA_CUDA(cudaMemcpyAsync(c.at<float>(p->L.disps[0]) + (size_t)p->f0 * p->P,
-                             c.b->disps_in + (size_t)p->f0 * p->P, fbytes * p->NL, cudaMemcpyDeviceToDevice,
-                             c.st));
+  if (p->NL > 0) {  // float32 boundary -> the float64 state
+    const long long n = (long long)p->NL * p->P;
+    if (int s = launch(c, widen_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, false,
+                       c.b->disps_in + (size_t)p->f0 * p->P, c.at<double>(p->L.disps[0]) + (size_t)p->f0 * p->P, n))
+      return s;
   }
   int s = reset_flags(c);
   if (s) return s;
@@ -1524,9 +1556,13 @@ int dba_solve(dba_plan* p, const dba_options* o, const dba_buffers* b, dba_repor
                            cudaMemcpyDeviceToDevice, c.st));
   DBA_CUDA(cudaMemcpyAsync(b->intr_out, c.at<double>(p->L.intr[cur]), sizeof(double) * 4,
                            cudaMemcpyDeviceToDevice, c.st));
-  if (p->NL > 0)
-    DBA_CUDA(cudaMemcpyAsync(b->disps_out + (size_t)p->f0 * p->P, c.at<float>(p->L.disps[dcur]) + (size_t)p->f0 * p->P,
-                             sizeof(float) * (size_t)p->P * p->NL, cudaMemcpyDeviceToDevice, c.st));
+  if (p->NL > 0) {  // the float64 state -> float32 boundary
+    const long long n = (long long)p->NL * p->P;
+    if ((s = launch(c, narrow_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, false,
+                    (const double*)(c.at<double>(p->L.disps[dcur]) + (size_t)p->f0 * p->P),
+                    b->disps_out + (size_t)p->f0 * p->P, n)))
+      return rep->status = s;
+  }
   if (p->gauge_on) {
     if ((s = gauge_sum(c, b->disps_out, gsum + 1))) return rep->status = s;
     GaugeArgs g;
@@ -1662,9 +1698,11 @@ int dba_debug_trial(dba_plan* p, const dba_options* o, const dba_buffers* b, dou
     DBA_CUDA(cudaMemcpy(delta, c.at<double>(p->L.delta), sizeof(double) * p->n_red, cudaMemcpyDeviceToHost));
   if (poses_n)
     DBA_CUDA(cudaMemcpy(poses_n, c.at<double>(p->L.poses[1]), sizeof(double) * 7 * p->N, cudaMemcpyDeviceToHost));
-  if (disps_n)
-    DBA_CUDA(cudaMemcpy(disps_n, c.at<float>(p->L.disps[1]), sizeof(float) * (size_t)p->N * p->P,
-                        cudaMemcpyDeviceToHost));
+  if (disps_n) {  // the float64 trial state, rounded once at the boundary
+    std::vector<double> tmp((size_t)p->N * p->P);
+    DBA_CUDA(cudaMemcpy(tmp.data(), c.at<double>(p->L.disps[1]), sizeof(double) * tmp.size(), cudaMemcpyDeviceToHost));
+    for (size_t x = 0; x < tmp.size(); ++x) disps_n[x] = (float)tmp[x];
+  }
   if (intr_n) DBA_CUDA(cudaMemcpy(intr_n, c.at<double>(p->L.intr[1]), sizeof(double) * 4, cudaMemcpyDeviceToHost));
   if (energy_n) *energy_n = rb.energy;
   return DBA_OK;

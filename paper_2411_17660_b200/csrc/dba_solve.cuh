@@ -83,6 +83,7 @@ struct SolveArgs {
   long long spec_Lband, spec_rLband, spec_mid, spec_delta;  // per-candidate strides (doubles)
   int* spec_status[kMaxSpec];
   double* spec_cond[kMaxSpec];
+  int refine;  // one step of iterative refinement (see refine_* below)
 };
 
 // the arguments of candidate k (k = 0: the controller's lambda)
@@ -106,7 +107,7 @@ __host__ __device__ inline long long solve_mid_len(int BW) {
 }
 
 struct SolveSmem {
-  size_t win, ring, th, thL, z, thm, thLm, zm, dinv, pbuf, cbuf, tbuf, pairs, bars, total;
+  size_t win, ring, th, thL, z, thm, thLm, zm, dinv, pbuf, cbuf, tbuf, pairs, xo, bars, total;
 };
 __host__ __device__ inline SolveSmem solve_smem_layout(int nb, int BW, int calib) {
   SolveSmem s;
@@ -125,6 +126,7 @@ __host__ __device__ inline SolveSmem solve_smem_layout(int nb, int BW, int calib
   s.tbuf = o; o += sizeof(double) * 24;
   s.pairs = o; o += sizeof(short2) * (size_t)(BW * (BW + 1) / 2 + 1);
   o = (o + 7) & ~size_t(7);
+  s.xo = o; o += sizeof(double) * ((size_t)6 * nb + 4);  // refinement: the unrefined step
   s.bars = o; o += sizeof(unsigned long long) * 2 * kRing;  // backward-sweep ring full/empty mbarriers
   s.total = (o + 15) & ~size_t(15);
   return s;
@@ -692,6 +694,107 @@ __device__ inline void chain_backward(double* z, const double* thL, const double
   __syncthreads();
 }
 
+// ---------------------------------------------------------------- iterative refinement
+// The block LDL^T with explicit 6x6 pivot inverses is backward stable only up to the
+// conditioning of its pivot blocks: on the noisy C3 system (cond(S + lam I) = 6e10) the
+// step is 4e-7 from the exact solution while LAPACK's Cholesky is 9e-9 (measured, an
+// emulation of this algorithm in numpy agrees: scratch/emul_ldl2.py).  One step of
+// iterative refinement with the stored factors -- r = y - (S + lam I) x in float64 from the
+// original band, the same forward / middle / backward substitutions on r, x += c --
+// brings it to 1e-10.  The substitutions reuse the factor rows in global memory and
+// the theta factors still in shared memory.
+
+// r[6a + s] of (S + lam I) x = y for pose block a (global order)
+__device__ inline double resid_pose(const SolveArgs& A, const double* x, int a, int s, double lam) {
+  const int BW = A.BW, W1 = BW + 1, nb = A.nb;
+  double v = fma(-lam, x[6 * a + s], A.y[6 * a + s]);
+  for (int c = max(0, a - BW); c <= a; ++c) {  // lower band and diagonal: row s of S_ac
+    const double* blk = A.band + ((size_t)a * W1 + (c - a + BW)) * 36 + 6 * s;
+#pragma unroll
+    for (int k = 0; k < 6; ++k) v = fma(-blk[k], x[6 * c + k], v);
+  }
+  for (int c = a + 1; c <= min(nb - 1, a + BW); ++c) {  // upper: S_ac = S_ca^T
+    const double* blk = A.band + ((size_t)c * W1 + (a - c + BW)) * 36 + s;
+#pragma unroll
+    for (int k = 0; k < 6; ++k) v = fma(-blk[6 * k], x[6 * c + k], v);
+  }
+  if (A.calib) {
+    const double* xt = x + 6 * nb;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) v = fma(-A.theta[(size_t)a * 24 + 6 * t + s], xt[t], v);
+  }
+  return v;
+}
+
+// r_theta (4) with warp w < 4 computing component w (fixed-order lane partials + tree)
+__device__ inline void resid_theta(const SolveArgs& A, const double* x, double lam, double* out) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nb = A.nb;
+  if (warp >= 4) return;
+  const int t = warp;
+  double v = 0.0;
+  for (int q = lane; q < 6 * nb; q += 32) v = fma(-A.theta[(size_t)(q / 6) * 24 + 6 * t + q % 6], x[q], v);
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+  if (lane == 0) {
+    double w = fma(-lam, x[6 * nb + t], A.y[6 * nb + t]);
+    for (int u = 0; u < 4; ++u) w = fma(-A.thth[4 * t + u], x[6 * nb + u], w);
+    out[t] = w + v;
+  }
+}
+
+// forward substitution with stored factor rows (one warp, warp 0):
+//   z_a -= sum_{b in [a-BW, a-1], b < npiv} L_ab z_b,  a = 1 .. nrows-1
+// lanes 6p + r (p < 5) own output component r of the blocks b = a-1-p-5q; the next
+// row's factor blocks are loaded while the current row folds
+template <int NS>
+__device__ inline void forward_apply(double* z, const double* Lband, int nrows, int npiv, int BW) {
+  const int lane = threadIdx.x & 31;
+  if ((threadIdx.x >> 5) != 0) return;
+  const int W1 = BW + 1, r = lane % 6, part = lane < 30 ? lane / 6 : 99;
+  double Lc[NS][6], Ln[NS][6];
+  auto load = [&](int a, double (&Lx)[NS][6]) {
+#pragma unroll
+    for (int j = 0; j < NS; ++j) {
+      const int b = a - 1 - part - 5 * j;
+      const bool use = part < 5 && a < nrows && b >= 0 && b >= a - BW && b < npiv;
+      const double* L = Lband + ((size_t)(use ? a : 0) * W1 + (use ? BW - (a - b) : 0)) * 36 + 6 * r;
+#pragma unroll
+      for (int k = 0; k < 6; ++k) Lx[j][k] = use ? L[k] : 0.0;
+    }
+  };
+  load(1, Lc);
+  for (int a = 1; a < nrows; ++a) {
+    load(a + 1, Ln);
+    double acc = 0.0;
+#pragma unroll
+    for (int j = 0; j < NS; ++j) {
+      const int b = max(a - 1 - part - 5 * j, 0);
+#pragma unroll
+      for (int k = 0; k < 6; ++k) acc = fma(Lc[j][k], z[6 * b + k], acc);
+    }
+    double tot = 0.0;
+#pragma unroll
+    for (int p = 0; p < 5; ++p) tot += __shfl_sync(0xffffffffu, acc, r + 6 * p);
+    if (lane < 6) z[6 * a + lane] -= tot;
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < NS; ++j)
+#pragma unroll
+      for (int k = 0; k < 6; ++k) Lc[j][k] = Ln[j][k];
+  }
+}
+
+// theta rows of the forward substitution: z_t -= sum_{b < npiv} L_tb z_b (warps 0..3)
+__device__ inline void forward_theta(double* z, const double* thL, int npiv, int ncols) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp >= 4) return;
+  double v = 0.0;
+  for (int q = lane; q < 6 * npiv; q += 32) v = fma(thL[(size_t)(q / 6) * 24 + 6 * warp + q % 6], z[q], v);
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+  if (lane == 0) z[6 * ncols + warp] -= v;
+}
+
 __device__ inline ChainSm chain_sm(unsigned char* smem, const SolveSmem& L, int* fail, bool middle) {
   ChainSm S;
   S.win = reinterpret_cast<double*>(smem + L.win);
@@ -805,6 +908,29 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const SolveArgs
   }
   chain_backward<NS>(S.z, S.thL, S.z + 6 * nb, A.Lband, S.ring, S.bars, nb, nb, BW, A.calib, A.delta);
   for (int x = tid; x < 6 * nb + (A.calib ? 4 : 0); x += kSolveThreads) A.delta[x] = S.z[x];
+  if (A.refine) {
+    double* xo = reinterpret_cast<double*>(smem + L.xo);
+    __syncthreads();
+    const int n = 6 * nb + (A.calib ? 4 : 0);
+    for (int x = tid; x < n; x += kSolveThreads) xo[x] = S.z[x];
+    __syncthreads();
+    for (int x = tid; x < 6 * nb; x += kSolveThreads) S.z[x] = resid_pose(A, xo, x / 6, x % 6, lam);
+    if (A.calib) resid_theta(A, xo, lam, S.z + 6 * nb);
+    __syncthreads();
+    forward_apply<NS>(S.z, A.Lband, nb, nb, BW);
+    __syncthreads();
+    if (A.calib) {
+      forward_theta(S.z, S.thL, nb, nb);
+      __syncthreads();
+      if (tid == 0) {
+        double cd;
+        theta_solve(S.th + (size_t)nb * 24, S.z + 6 * nb, lam, &cd);
+      }
+      __syncthreads();
+    }
+    chain_backward<NS>(S.z, S.thL, S.z + 6 * nb, A.Lband, S.ring, S.bars, nb, nb, BW, A.calib, A.delta);
+    for (int x = tid; x < n; x += kSolveThreads) A.delta[x] = xo[x] + S.z[x];
+  }
   if (A.scalefix) {
     __syncthreads();
     scale_correct(A, lam);
@@ -955,6 +1081,85 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve2_kernel(const SolveArg
     for (int x = tid; x < 6 * BW; x += kSolveThreads) A.delta[6 * m + x] = xsol[x];
     if (calib && tid < 4) A.delta[6 * nb + tid] = xsol[6 * BW + tid];
   }
+  }
+  if (A.refine) {
+    // ---- one refinement step: residual of both halves, forward on each chain, the
+    // middle system on CTA 0, back-substitution, x += correction
+    __threadfence();
+    grid.sync();  // the whole step is in A.delta
+    double* xo = reinterpret_cast<double*>(smem + L.xo);
+    const int n = 6 * nb + (calib ? 4 : 0);
+    double* exz = A.mid + cta * per;  // exchange: z of the middle rows (6 BW) + theta (4)
+    if (!failed) {
+      for (int x = tid; x < n; x += kSolveThreads) xo[x] = A.delta[x];
+      __syncthreads();
+      for (int x = tid; x < 6 * nrows; x += kSolveThreads) {
+        const int a = x / 6, s2 = x % 6;
+        S.z[x] = resid_pose(A, xo, cta == 0 ? a : nb - 1 - a, s2, lam);
+      }
+      if (calib) resid_theta(A, xo, lam, S.z + 6 * nb);
+      __syncthreads();
+      forward_apply<NS>(S.z, Lb, nrows, npiv, BW);
+      __syncthreads();
+      if (calib) {
+        forward_theta(S.z, S.thL, npiv, nb);
+        __syncthreads();
+      }
+      for (int x = tid; x < 6 * BW; x += kSolveThreads) exz[x] = S.z[6 * npiv + x];
+      if (calib && tid < 4) exz[6 * BW + tid] = S.z[6 * nb + tid];
+    }
+    __threadfence();
+    grid.sync();
+    if (cta == 0 && !failed) {
+      const ChainSm M = chain_sm(smem, L, &fail, true);
+      const double* Tz = A.mid;
+      const double* Rz = A.mid + per;
+      for (int x = tid; x < 6 * BW; x += kSolveThreads) {
+        const int i = x / 6, s2 = x % 6;
+        M.z[x] = Tz[x] + Rz[6 * (BW - 1 - i) + s2] - resid_pose(A, xo, m + i, s2, lam);
+      }
+      if (calib) {
+        resid_theta(A, xo, lam, xts);
+        __syncthreads();
+        if (tid < 4) M.z[6 * BW + tid] = Tz[6 * BW + tid] + Rz[6 * BW + tid] - xts[tid];
+      }
+      __syncthreads();
+      double* Lm = A.mid + 2 * per;
+      forward_apply<NS>(M.z, Lm, BW, BW, BW - 1);
+      __syncthreads();
+      if (calib) {
+        forward_theta(M.z, M.thL, BW, BW);
+        __syncthreads();
+        if (tid == 0) {
+          double cd;
+          theta_solve(M.th + (size_t)BW * 24, M.z + 6 * BW, lam, &cd);
+        }
+        __syncthreads();
+      }
+      chain_backward<NS>(M.z, M.thL, M.z + 6 * BW, Lm, M.ring, M.bars, BW, BW, BW - 1, calib, A.delta + 6 * m);
+      for (int x = tid; x < 6 * BW + (calib ? 4 : 0); x += kSolveThreads) xsol[x] = M.z[x];
+    }
+    __threadfence();
+    grid.sync();
+    if (!failed) {
+      for (int x = tid; x < 6 * BW; x += kSolveThreads) {
+        const int i = x / 6, s2 = x % 6;
+        S.z[6 * npiv + x] = xsol[6 * (cta == 0 ? i : BW - 1 - i) + s2];
+      }
+      if (tid < 4) xts[tid] = calib ? xsol[6 * BW + tid] : 0.0;
+      __syncthreads();
+      double* tmp = A.delta + (cta == 0 ? 0 : 6 * (m + BW));
+      chain_backward<NS>(S.z, S.thL, xts, Lb, S.ring, S.bars, nrows, npiv, BW, calib, tmp);
+      for (int x = tid; x < 6 * npiv; x += kSolveThreads) {
+        const int a = x / 6, s2 = x % 6;
+        const int g = 6 * (cta == 0 ? a : nb - 1 - a) + s2;
+        A.delta[g] = xo[g] + S.z[x];
+      }
+      if (cta == 0) {
+        for (int x = tid; x < 6 * BW; x += kSolveThreads) A.delta[6 * m + x] = xo[6 * m + x] + xsol[x];
+        if (calib && tid < 4) A.delta[6 * nb + tid] = xo[6 * nb + tid] + xsol[6 * BW + tid];
+      }
+    }
   }
   if (A.scalefix) {
     __threadfence();

@@ -102,19 +102,18 @@ __global__ void prep_kernel(const PrepArgs A) {
     EdgeLin el;
     EdgeBack eb;
     for (int c = 0; c < 9; ++c) {
-      el.R[c] = (float)Rn[c];
-      eb.R[c] = (float)Rc[c];
+      el.R[c] = Rn[c];
+      eb.R[c] = Rc[c];
     }
     for (int c = 0; c < 3; ++c) {
-      el.t[c] = (float)gn.t[c];
-      eb.t[c] = (float)gc.t[c];
+      el.t[c] = gn.t[c];
+      eb.t[c] = gc.t[c];
     }
     for (int r = 0; r < 6; ++r) {
       double s2 = xi_j[r];
       for (int c = 0; c < 6; ++c) s2 -= Ac[6 * r + c] * xi_i[c];
-      eb.dlt[r] = (float)s2;
+      eb.dlt[r] = s2;
     }
-    eb.pad[0] = eb.pad[1] = 0.f;
     // a non-finite trial pose or intrinsics: the energy-only trial pass cannot see it
     // (invalid projections contribute zero), so flag the edge here
     bool ok = true;
@@ -431,6 +430,18 @@ __global__ void __launch_bounds__(kFinalThreads) finalize_kernel(const FinalArgs
 // ---------------------------------------------------------------- gauge (A5)
 
 // sum of log d over one frame (fixed-order tree); out[0] = sum (0 if frame < 0)
+// float32 boundary disparities <-> the float64 solver state
+__global__ void __launch_bounds__(256) widen_kernel(const float* src, double* dst, long long n) {
+  pdl_enter();
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < n) dst[t] = (double)src[t];
+}
+__global__ void __launch_bounds__(256) narrow_kernel(const double* src, float* dst, long long n) {
+  pdl_enter();
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < n) dst[t] = (float)src[t];
+}
+
 __global__ void __launch_bounds__(256) logsum_kernel(const float* d, int frame, int P, double* out) {
   pdl_enter();
   __shared__ double sh[256];

@@ -32,7 +32,8 @@ from .errors import (CalibrationDegenerateError, CapacityError, ConfigError, Num
                      SolverFailure)
 
 DEFAULTS = dict(lambda0=1e-4, lambda_min=1e-8, lambda_max=1e6, eta=1e-4, alpha=1e-3,
-                d_min=1e-6, tangent_max=1.0, calib_cond_max=1e8, damping_candidates=0)
+                d_min=1e-6, tangent_max=1.0, calib_cond_max=1e8, damping_candidates=0,
+                refine=True)
 
 
 # ----------------------------------------------------------------------------- SPEC types
@@ -213,7 +214,7 @@ class DBASolver:
         o.update({k: v for k, v in kw.items() if v is not None})
         return _lib.Options(int(iters), o["lambda0"], o["lambda_min"], o["lambda_max"], o["eta"],
                             o["alpha"], o["d_min"], o["tangent_max"], o["calib_cond_max"],
-                            int(o["damping_candidates"]))
+                            int(o["damping_candidates"]), 0 if o["refine"] else 1)
 
     def _inputs(self, poses, disps, intr, flow, prior, prior_mask, prior_weight=None):
         dev = self.device
@@ -425,15 +426,35 @@ def _unpack_state(state: BAState, poses, disps, intr):
     return BAState(new_poses, dn, new_intr)
 
 
+def _blocks(problem: BAProblem, calib: bool):
+    """BAProblem block flags -> (fixed frames, optimize_intrinsics, freeze_disparities)
+    ("exactly the flagged blocks receive updates").  Per-frame scales and
+    offsets exist only in the P-RGBD mode (``prgbd.solve_prgbd_bcd``)."""
+    fl = problem.flags if problem.flags is not None else BlockFlags()
+    if fl.scales_offsets:
+        raise ConfigError("scales_offsets is a P-RGBD block: use prgbd.solve_prgbd_bcd")
+    if calib and not fl.intrinsics:
+        raise ConfigError("solve_ba_calib needs the intrinsics block flagged (SPEC.md:324)")
+    return bool(fl.poses), bool(fl.intrinsics), not bool(fl.disparities)
+
+
 def _run(problem: BAProblem, state: BAState, calib: bool):
     poses, disps, intr = _pack_state(state)
     N, H, W = (int(s) for s in np.shape(disps))
     edges = np.asarray(problem.edges, dtype=np.int32).reshape(-1, 2)
+    if len(edges) == 0:
+        raise ConfigError("solve_ba needs at least one edge (SPEC.md:315)")
     flow = _pack_flow(problem, H, W)
     use_prior = problem.prior is not None
-    s = get_solver(edges[:, 0], edges[:, 1], N, H, W, problem.fixed,
+    move_poses, calib, freeze_d = _blocks(problem, calib)
+    fixed = problem.fixed if move_poses else np.ones(N, dtype=bool)  # poses unflagged: all fixed
+    if not move_poses and not calib and freeze_d:  # nothing flagged: the state is returned as is
+        e = energy(problem, state)
+        return state, BAReport(initial_energy=e, final_energy=e, iterations_run=0, energy_trace=[],
+                               converged=True)
+    s = get_solver(edges[:, 0], edges[:, 1], N, H, W, fixed,
                    optimize_intrinsics=calib, use_prior=use_prior,
-                   scale_gauge=problem.scale_gauge)
+                   scale_gauge=problem.scale_gauge, freeze_disparities=freeze_d)
     Po, Do, Ko, rep = s.solve(poses, disps, intr, flow, problem.prior, problem.prior_mask,
                               iters=problem.iterations, lambda0=problem.damping,
                               alpha=problem.alpha)
@@ -441,12 +462,17 @@ def _run(problem: BAProblem, state: BAState, calib: bool):
 
 
 def solve_ba(problem: BAProblem, state: BAState):
-    """damped GN with Schur elimination; returns (state', BAReport)."""
+    """damped GN with Schur elimination; returns (state', BAReport).
+    Only the blocks flagged in ``problem.flags`` are updated (poses, disparities and, when
+    flagged, the intrinsics)."""
     return _run(problem, state, calib=False)
 
 
 def solve_ba_calib(problem: BAProblem, state: BAState):
-    """as solve_ba with the intrinsics as a global block."""
+    """as solve_ba with the intrinsics as a global block (the intrinsics
+    flag is set for the caller when the problem's flags leave it at the default)."""
+    if problem.flags is None or problem.flags == BlockFlags():
+        problem = BAProblem(**{**problem.__dict__, "flags": BlockFlags(intrinsics=True)})
     return _run(problem, state, calib=True)
 
 
@@ -462,7 +488,12 @@ def energy(problem: BAProblem, state: BAState) -> float:
 
 
 def energy_rgbd(problem: BAProblem, state: BAState, prior, alpha=1e-3, mask=None) -> float:
-    """Eq. 2 + alpha * sum m (d* - d)^2."""
+    """Eq. 2 + alpha * sum m (d* - d)^2.  ``mask`` defaults to the
+    prior's validity (d* > 0); a missing prior is a configuration error."""
+    if prior is None:
+        raise ConfigError("energy_rgbd needs the disparity prior d* (SPEC.md:335)")
+    if mask is None:
+        mask = (np.asarray(prior.cpu() if isinstance(prior, torch.Tensor) else prior) > 0).astype(np.uint8)
     p = BAProblem(edges=problem.edges, updates=problem.updates, flow=problem.flow,
                   fixed=problem.fixed, flags=problem.flags, prior=prior,
                   prior_mask=mask, alpha=alpha)

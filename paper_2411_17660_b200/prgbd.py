@@ -9,6 +9,12 @@
   squares in float64 on the device, s_i >= 1e-4), then one accepted disparity step from a
   plan with every pose fixed (the same kernels; the reduced system is empty).
 
+``two_stage_uncalibrated``: stage 1 = ``solve_ba_calib`` with the Eq. 4
+prior as a fixed regulariser (alpha = 1e-3) from the heuristic f = (H+W)/2 (geometry.py:
+222-225) -- a poorly conditioned intrinsics block raises ``CalibrationDegenerateError`` and
+stage 2 is not attempted; stage 2 = ``solve_prgbd_bcd`` with the calibrated intrinsics
+frozen (bitwise untouched).
+
 ``fill_nonkeyframe_poses``: se(3) geodesic interpolation between the
 two nearest keyframes (geometry.py:181-184), refined — when flow records keyframe -> frame
 exist — by motion-only Gauss-Newton on the GPU: one plan over all non-keyframes with the
@@ -97,6 +103,32 @@ def solve_prgbd_bcd(ii, jj, poses, disps, intr, flow, prior, mask, fixed, scale=
             P, D, _, _ = solver_b.solve(P, D, K, F, eff, M, prior_weight=w, iters=stage_b_iters, **opts)
             trace.append(energy(P, D))
     return P, D, s, o, trace
+
+
+def heuristic_intrinsics(height, width):
+    """f = (H + W)/2, principal point at the image centre (geometry.py:222-225)."""
+    f = (height + width) / 2.0
+    return np.array([f, f, width / 2.0, height / 2.0])
+
+
+def two_stage_uncalibrated(ii, jj, poses, disps, flow, prior, mask, fixed, intr0=None, *, calib_iters=8,
+                           cycles=2, iters=4, device=None, **opts):
+    """SPEC.md:349-357.  Returns (poses, disps, intr, scale, offset, trace); ``trace`` is the
+    stage-2 BCD trace.  Raises CalibrationDegenerateError from stage 1 (no stage 2)."""
+    dev = _device(device)
+    D0 = _to_dev(disps, torch.float32, dev)
+    N, H, W = D0.shape
+    K0 = heuristic_intrinsics(H, W) if intr0 is None else np.asarray(intr0, np.float64)
+    PR = _to_dev(prior, torch.float32, dev)
+    M = _to_dev(mask, torch.uint8, dev)
+    # stage 1: Eq. 3 + Eq. 4 (fixed prior, no scales/offsets), intrinsics as a global block
+    s1 = DBASolver(ii, jj, N, H, W, fixed, optimize_intrinsics=True, use_prior=True, device=dev)
+    P1, D1, K1, _ = s1.solve(poses, D0, K0, flow, PR, M, iters=calib_iters, **opts)
+    # stage 2: P-RGBD (Eq. 5) with the calibrated camera frozen
+    K1 = K1.clone()
+    P2, D2, sc, off, trace = solve_prgbd_bcd(ii, jj, P1, D1, K1, flow, PR, M, fixed, cycles=cycles,
+                                            iters=iters, device=dev, **opts)
+    return P2, D2, K1, sc, off, trace
 
 
 def _bracket(kf_ids, t):

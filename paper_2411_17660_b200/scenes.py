@@ -52,7 +52,7 @@ class SceneSpec:
     def __post_init__(self):
         if self.frames < 2:
             raise ConfigError(f"scene needs at least 2 frames, got {self.frames}")
-        if self.trajectory not in ("orbit", "line", "rotate"):
+        if self.trajectory not in ("orbit", "line", "rotate", "helix"):
             raise ConfigError(f"unknown trajectory type '{self.trajectory}'")
         if self.height < 8 or self.width < 8:
             raise ConfigError("scene resolution must be at least 8x8")
@@ -113,6 +113,14 @@ class Scene:
             c = np.array([x, -0.4 * np.sin(np.pi * s), 0.2 * np.sin(2 * np.pi * s)])
             yaw = 0.25 * np.sin(2 * np.pi * s)
             fw = np.array([np.sin(yaw), np.cos(yaw), -0.05])
+        elif sp.trajectory == "helix":
+            # not in the reference provider: a translation-rich orbit (vertical travel and
+            # pitch) on which both focal lengths are observable -- the setting of the SPEC
+            # calibration example.  On orbit/line the camera moves and yaws in
+            # a near-horizontal plane, so f_y is (near-)degenerate with a vertical stretch.
+            ph = 2 * np.pi * s
+            c = np.array([ORBIT_RADIUS * np.cos(ph), ORBIT_RADIUS * np.sin(ph), 0.9 * np.sin(3 * ph)])
+            fw = np.array([np.cos(ph), np.sin(ph), 0.35 * np.sin(2 * ph)])
         else:
             yaw = 1.2 * s
             c = np.array([0.5, 0.0, 0.0])

@@ -19,13 +19,9 @@ pytestmark = pytest.mark.gpu
 REL_TOL = 1e-4
 
 
-def _disp_err(d, d_ref, d_prev):
-    """Disparity error relative to the state magnitude max(d_ref, d_prev).
-
-    Equal to |d - d_ref| / d_ref except for pixels that a step drives towards zero
-    disparity, where the fp32 back-substitution's absolute error (which scales with
-    the step, not with the tiny result) is measured against the step's origin."""
-    return np.abs(d - d_ref) / np.maximum(d_ref, d_prev)
+def _disp_err(d, d_ref, d_prev=None):
+    """Disparity error relative to the oracle's value: |d - d_ref| / d_ref."""
+    return np.abs(d - d_ref) / d_ref
 
 
 @pytest.fixture(scope="module")
@@ -181,9 +177,8 @@ def test_solve_parity_calib(torch_cuda, iters):
     assert np.abs(Ko.cpu().numpy() - ref.intr).max() / np.abs(ref.intr).max() < REL_TOL
     te, ae = pose_errors(Po.cpu().numpy(), ref.poses)
     assert te < REL_TOL, te
-    rel = _disp_err(Do.cpu().numpy().astype(np.float64), ref.disps, wl.disps0)
-    assert np.quantile(rel, 0.999) < REL_TOL, np.quantile(rel, 0.999)
-    assert rel.max() < 10 * REL_TOL, rel.max()
+    rel = _disp_err(Do.cpu().numpy().astype(np.float64), ref.disps)
+    assert rel.max() < REL_TOL, rel.max()
 
 
 @pytest.mark.parametrize("calib,keyframes,radius", [(False, 40, 2), (True, 40, 2), (False, 48, 3)])
@@ -286,7 +281,10 @@ def test_full_size_c3_properties(torch_cuda):
     s = dba.DBASolver(wl.ii, wl.jj, len(wl.frames), 48, 64, wl.fixed)
     Po, Do, Ko, rep = s.solve(wl.poses0, wl.disps0, wl.intr0, wl.flow, iters=8)
     P, D = Po.cpu().numpy(), Do.cpu().numpy()
-    assert rep.iterations_run == 8
+    # noiseless: the energy reaches the float64 floor of the float32 flow targets
+    # (~1e-13 of the initial energy) after 4-5 iterations; later trials tie at that floor
+    # and the controller may stop early, converged
+    assert rep.iterations_run == 8 or (rep.converged and rep.iterations_run >= 5)
     tr = [rep.initial_energy] + list(rep.energy_trace)
     assert all(b <= a for a, b in zip(tr, tr[1:]))
     assert rep.final_energy < 1e-9 * rep.initial_energy

@@ -183,7 +183,7 @@ def test_gpu_bcd_parity():
     te, ae = pose_errors(P.cpu().numpy(), ref.poses)
     assert te < REL and ae < 1e-3
     rel = np.abs(D.cpu().numpy() - ref.disps) / ref.disps
-    assert rel.max() < 10 * REL and np.quantile(rel, 0.999) < REL
+    assert rel.max() < REL, rel.max()
     assert np.allclose(s.cpu().numpy(), rs, rtol=REL) and np.allclose(o.cpu().numpy(), ro, atol=REL)
     # both blocks frozen: a no-op
     P2, D2, *_ = prgbd.solve_prgbd_bcd(ii, jj, p0, d0, sc.intr, flow, prior, mask, fixed,
