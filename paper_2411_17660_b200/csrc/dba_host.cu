@@ -377,7 +377,7 @@ int dba_plan_create(const dba_problem_desc* d, dba_plan** out) {
     }
     p->pass_smem = s.total;
     const int mb = pass_mb(pass_mpad(std::max(p->kmax, 1), p->calib));
-    p->mb = mb <= 6 ? 6 : 12;
+    p->mb = mb <= 5 ? 5 : mb <= 6 ? 6 : 12;  // 5: radius-5 graphs (k = 10); 6: with intrinsics
     if (p->pass_smem > 225 * 1024 || mb > 12) {
       delete p;
       return DBA_ECAPACITY;
@@ -1001,8 +1001,11 @@ int launch_pass(Ctx& c, int cur, int nxt, bool backsub, bool system, bool gated 
   a.seg_off_edge = c.at<long long>(p->L.seg_off_edge);
   a.seg_off_M = c.at<long long>(p->L.seg_off_M);
   a.seg_off_w = c.at<long long>(p->L.seg_off_w);
-  if (p->calib) return p->mb == 6 ? launch_pass_t<true, 6>(c, a) : launch_pass_t<true, 12>(c, a);
-  return p->mb == 6 ? launch_pass_t<false, 6>(c, a) : launch_pass_t<false, 12>(c, a);
+  if (p->calib)
+    return p->mb == 5 ? launch_pass_t<true, 5>(c, a) : p->mb == 6 ? launch_pass_t<true, 6>(c, a)
+                                                             : launch_pass_t<true, 12>(c, a);
+  return p->mb == 5 ? launch_pass_t<false, 5>(c, a) : p->mb == 6 ? launch_pass_t<false, 6>(c, a)
+                                                            : launch_pass_t<false, 12>(c, a);
 }
 
 // LM controller inputs: the trial (slot 1) energy, the flags word and the options

@@ -275,8 +275,9 @@ __global__ void __launch_bounds__(kPassThreads, 1) pass_kernel(const PassArgs A)
     const int per = (nblk + kPassWarps - 1) / kPassWarps;
     const int bq0 = min(warp * per, nblk), nmine = min(per, nblk - bq0);
     int offA[MB], offB[MB];
+    unsigned reuseA = 0, diag = 0;  // per block: A fragment = the previous block's / B = A
     {
-      int bi = 0, rowlen = nb8, b = bq0;
+      int bi = 0, rowlen = nb8, b = nmine > 0 ? bq0 : 0;  // idle warps: any valid block
       while (b >= rowlen) {
         b -= rowlen;
         ++bi;
@@ -287,6 +288,8 @@ __global__ void __launch_bounds__(kPassThreads, 1) pass_kernel(const PassArgs A)
       for (int q = 0; q < MB; ++q) {
         offA[q] = (8 * bi + (lane >> 2)) * US + (lane & 3);
         offB[q] = (8 * bj + (lane >> 2)) * US + (lane & 3);
+        if (q > 0 && offA[q] == offA[q - 1]) reuseA |= 1u << q;
+        if (bi == bj) diag |= 1u << q;
         if (++bj == nb8) {
           ++bi;
           bj = bi;
@@ -559,7 +562,30 @@ __global__ void __launch_bounds__(kPassThreads, 1) pass_kernel(const PassArgs A)
       __syncthreads();
       // ------------------------------------------------------------ phase C (K3a)
       // M_ext += V V^T: a warp's blocks, k-steps of 4 pixels, fragments straight from U
-      if (nmine > 0) {
+      if (nmine == MB) {
+        // the common case: every block slot used, so the k-loop has no predication
+        // (no per-MMA warp re-convergence) and A fragments shared by consecutive blocks
+        // of one row, and B = A on diagonal blocks, are loaded once
+        for (int p0 = 0; p0 < SUB; p0 += 32) {
+#pragma unroll
+          for (int kk = 0; kk < 32; kk += 4) {
+            double av[MB], bv[MB];
+#pragma unroll
+            for (int q = 0; q < MB; ++q) {
+              if ((reuseA >> q) & 1u)
+                av[q] = av[q > 0 ? q - 1 : 0];
+              else
+                av[q] = U[offA[q] + p0 + kk];
+              if ((diag >> q) & 1u)
+                bv[q] = av[q];
+              else
+                bv[q] = U[offB[q] + p0 + kk];
+            }
+#pragma unroll
+            for (int q = 0; q < MB; ++q) dmma884(macc[q], av[q], bv[q]);
+          }
+        }
+      } else if (nmine > 0) {
 #pragma unroll 2
         for (int p0 = 0; p0 < SUB; p0 += 4) {
 #pragma unroll
