@@ -98,7 +98,7 @@ struct dba_plan {
   int calib = 0, prior = 0, freeze_d = 0, gauge_on = 0, gauge_frame = -1, rank = 0, nranks = 1;
   int scalefix = 0, anchor = -1;  // prior-fixed monocular scale: exact-row step correction
   int f0 = 0, f1 = 0, NL = 0, EL = 0, kmax = 0, nb = 0, BW = 0, n_red = 0;
-  int n_tiles = 0, G = 0, nseg = 0, n_units = 0, nve = kEdgeVals, sub = 128, mb = 6;
+  int n_tiles = 0, G = 0, nseg = 0, n_units = 0, nve = kEdgeVals, sub = 128, mb = 6, ring = 32;
   size_t pass_smem = 0, solve_smem = 0;
   long long sys_len = 0;  // doubles in one packed reduced system
   long long spec_delta = 0, spec_Lband = 0, spec_rLband = 0, spec_mid = 0;  // per damping candidate
@@ -119,6 +119,7 @@ struct dba_plan {
   int two_sided = 0, m_top = 0;  // two-CTA solve: pivots of the top chain
   std::vector<int> fixed_ridx;
   std::vector<int> block_pose;  // reduced block -> pose
+  std::vector<int> natural_of_block;  // reduced block -> index among the free poses in pose order
   std::vector<int> local_edges;  // input edge id of each local flow row
   Layout L{};
   std::vector<unsigned char> meta;  // image of [0, meta_end)
@@ -314,18 +315,11 @@ int dba_plan_create(const dba_problem_desc* d, dba_plan** out) {
       }
   }
 
-  // ---- reduced variables: free poses in index order, theta last
-  p->fixed_ridx.assign(N, -1);
-  int nfree = 0;
-  for (int k = 0; k < N; ++k)
-    if (!d->fixed[k]) p->fixed_ridx[k] = nfree++;
-  p->nb = nfree;
-  p->n_red = 6 * nfree + 4 * p->calib;
-  p->block_pose.assign(std::max(nfree, 1), 0);
-  for (int k = 0; k < N; ++k)
-    if (p->fixed_ridx[k] >= 0) p->block_pose[p->fixed_ridx[k]] = k;
-  // band width from the fill-in pattern of every source frame
-  std::vector<std::vector<int>> vars(N);
+  // ---- reduced variables: free poses, theta last.  The block order is the natural one
+  // unless a reverse Cuthill-McKee order of the fill-in graph gives a narrower band: a
+  // loop-closure edge (e.g. 0 <-> 299 on a 300-frame chain) makes the natural band span
+  // the whole chain, while RCM folds the cycle (band 20 blocks instead of 298).
+  std::vector<std::vector<int>> vars(N);  // each source frame's local variables
   for (int k = 0; k < N; ++k) vars[k].push_back(k);
   {
     std::vector<int> order(E);
@@ -334,13 +328,94 @@ int dba_plan_create(const dba_problem_desc* d, dba_plan** out) {
                      [&](int a, int b) { return d->ii[a] < d->ii[b]; });
     for (int e : order) vars[d->ii[e]].push_back(d->jj[e]);
   }
-  int BW = 0;
+  auto band_of = [&](const std::vector<int>& ridx) {
+    int B = 0;
+    for (int k = 0; k < N; ++k) {
+      int lo = INT_MAX, hi = -1;
+      for (int a : vars[k])
+        if (ridx[a] >= 0) {
+          lo = std::min(lo, ridx[a]);
+          hi = std::max(hi, ridx[a]);
+        }
+      if (hi >= 0) B = std::max(B, hi - lo);
+    }
+    return B;
+  };
+  p->fixed_ridx.assign(N, -1);
+  int nfree = 0;
   for (int k = 0; k < N; ++k)
-    for (int a : vars[k])
-      for (int c : vars[k]) {
-        const int ra = p->fixed_ridx[a], rc = p->fixed_ridx[c];
-        if (ra >= 0 && rc >= 0) BW = std::max(BW, std::abs(ra - rc));
+    if (!d->fixed[k]) p->fixed_ridx[k] = nfree++;
+  p->natural_of_block.resize(std::max(nfree, 1));
+  for (int k = 0; k < N; ++k)
+    if (p->fixed_ridx[k] >= 0) p->natural_of_block[p->fixed_ridx[k]] = p->fixed_ridx[k];
+  int BW = band_of(p->fixed_ridx);
+  if (BW > 1 && nfree > 2) {
+    std::vector<std::set<int>> adj(N);
+    for (int k = 0; k < N; ++k)
+      for (int a : vars[k])
+        for (int c : vars[k])
+          if (a != c && !d->fixed[a] && !d->fixed[c]) adj[a].insert(c);
+    auto deg_less = [&](int a, int b) {
+      return adj[a].size() != adj[b].size() ? adj[a].size() < adj[b].size() : a < b;
+    };
+    std::vector<int> free_sorted;
+    for (int k = 0; k < N; ++k)
+      if (!d->fixed[k]) free_sorted.push_back(k);
+    std::stable_sort(free_sorted.begin(), free_sorted.end(), deg_less);
+    // starts: the lowest-degree (peripheral) poses and the first / last free pose
+    std::vector<int> starts(free_sorted.begin(), free_sorted.begin() + std::min<size_t>(4, free_sorted.size()));
+    starts.push_back(free_sorted.front());
+    for (int k = 0; k < N; ++k)
+      if (!d->fixed[k]) {
+        starts.push_back(k);
+        break;
       }
+    for (int k = N - 1; k >= 0; --k)
+      if (!d->fixed[k]) {
+        starts.push_back(k);
+        break;
+      }
+    for (int s0 : starts) {
+      std::vector<char> seen(N, 0);
+      std::vector<int> order;
+      auto bfs = [&](int root) {
+        std::vector<int> q{root};
+        seen[root] = 1;
+        for (size_t h = 0; h < q.size(); ++h) {
+          const int u = q[h];
+          order.push_back(u);
+          std::vector<int> nb(adj[u].begin(), adj[u].end());
+          std::stable_sort(nb.begin(), nb.end(), deg_less);
+          for (int w : nb)
+            if (!seen[w]) {
+              seen[w] = 1;
+              q.push_back(w);
+            }
+        }
+      };
+      bfs(s0);
+      for (int k : free_sorted)
+        if (!seen[k]) bfs(k);
+      std::vector<int> ridx(N, -1);
+      for (size_t i = 0; i < order.size(); ++i) ridx[order[order.size() - 1 - i]] = (int)i;
+      const int B2 = band_of(ridx);
+      if (B2 < BW) {
+        BW = B2;
+        std::vector<int> nat(N, -1);
+        int c2 = 0;
+        for (int k = 0; k < N; ++k)
+          if (!d->fixed[k]) nat[k] = c2++;
+        p->fixed_ridx = ridx;
+        for (int k = 0; k < N; ++k)
+          if (ridx[k] >= 0) p->natural_of_block[ridx[k]] = nat[k];
+      }
+    }
+  }
+  p->nb = nfree;
+  p->n_red = 6 * nfree + 4 * p->calib;
+  p->block_pose.assign(std::max(nfree, 1), 0);
+  for (int k = 0; k < N; ++k)
+    if (p->fixed_ridx[k] >= 0) p->block_pose[p->fixed_ridx[k]] = k;
   p->BW = (p->nb > 0) ? std::min(BW, p->nb - 1) : 0;
   const int W1 = p->BW + 1;
   p->band_len = (long long)p->nb * W1 * 36;
@@ -358,9 +433,16 @@ int dba_plan_create(const dba_problem_desc* d, dba_plan** out) {
 
   // ---- solve kernel shared memory
   {
-    const SolveSmem s = solve_smem_layout(p->nb, p->BW, p->calib);
+    // the backward sweep's factor-row ring: 32 rows, or 8 when a wide band (a folded
+    // loop closure) would not fit otherwise
+    p->ring = kRing;
+    SolveSmem s = solve_smem_layout(p->nb, p->BW, p->calib, kRing);
+    if (s.total > 200 * 1024) {
+      p->ring = kRingWide;
+      s = solve_smem_layout(p->nb, p->BW, p->calib, kRingWide);
+    }
     p->solve_smem = s.total;
-    if (p->solve_smem > 200 * 1024 || p->BW > kMaxBand) {
+    if (p->solve_smem > 225 * 1024 || p->BW > kMaxBand) {
       delete p;
       return DBA_ECAPACITY;
     }
@@ -1228,10 +1310,17 @@ int launch_solve(Ctx& c, int slot, int nspec = 1) {
     a.spec_cond[k] = cand_cond(c, k);
   }
   void (*kern)(const SolveArgs);
+  const bool wide = p->ring != kRing;
   if (p->two_sided)
-    kern = (p->BW <= 5) ? solve2_kernel<1> : (p->BW <= 10) ? solve2_kernel<2> : solve2_kernel<5>;
+    kern = wide ? ((p->BW <= 5) ? solve2_kernel<1, kRingWide> : (p->BW <= 10) ? solve2_kernel<2, kRingWide>
+                                                                        : solve2_kernel<5, kRingWide>)
+                : ((p->BW <= 5) ? solve2_kernel<1, kRing> : (p->BW <= 10) ? solve2_kernel<2, kRing>
+                                                                    : solve2_kernel<5, kRing>);
   else
-    kern = (p->BW <= 5) ? solve_kernel<1> : (p->BW <= 10) ? solve_kernel<2> : solve_kernel<5>;
+    kern = wide ? ((p->BW <= 5) ? solve_kernel<1, kRingWide> : (p->BW <= 10) ? solve_kernel<2, kRingWide>
+                                                                       : solve_kernel<5, kRingWide>)
+                : ((p->BW <= 5) ? solve_kernel<1, kRing> : (p->BW <= 10) ? solve_kernel<2, kRing>
+                                                                   : solve_kernel<5, kRing>);
   DBA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->solve_smem));
   auto& pr = p->prof;
   std::pair<int, int> ev{-1, -1};
@@ -1657,10 +1746,11 @@ int dba_build_system(dba_plan* p, const dba_options* o, const dba_buffers* b, do
       const int cb = a - p->BW + pos;
       if (cb < 0) continue;
       const double* blk = sys.data() + ((size_t)a * W1 + pos) * 36;
+      const int na = p->natural_of_block[a], nc = p->natural_of_block[cb];  // natural order
       for (int r = 0; r < 6; ++r)
         for (int q = 0; q < 6; ++q) {
-          S[(size_t)(6 * a + r) * n + 6 * cb + q] = blk[6 * r + q];
-          S[(size_t)(6 * cb + q) * n + 6 * a + r] = blk[6 * r + q];
+          S[(size_t)(6 * na + r) * n + 6 * nc + q] = blk[6 * r + q];
+          S[(size_t)(6 * nc + q) * n + 6 * na + r] = blk[6 * r + q];
         }
     }
   if (p->calib) {
@@ -1669,13 +1759,15 @@ int dba_build_system(dba_plan* p, const dba_options* o, const dba_buffers* b, do
       for (int t = 0; t < 4; ++t)
         for (int q = 0; q < 6; ++q) {
           const double v = sys[p->theta_off + (size_t)cb * 24 + 6 * t + q];
-          S[(size_t)(t0 + t) * n + 6 * cb + q] = v;
-          S[(size_t)(6 * cb + q) * n + t0 + t] = v;
+          const int nc = p->natural_of_block[cb];
+          S[(size_t)(t0 + t) * n + 6 * nc + q] = v;
+          S[(size_t)(6 * nc + q) * n + t0 + t] = v;
         }
     for (int t = 0; t < 4; ++t)
       for (int u = 0; u < 4; ++u) S[(size_t)(t0 + t) * n + t0 + u] = sys[p->thth_off + 4 * t + u];
   }
-  for (int x = 0; x < n; ++x) y[x] = sys[p->y_off + x];
+  for (int x = 0; x < n; ++x)
+    y[x < 6 * p->nb ? 6 * p->natural_of_block[x / 6] + x % 6 : x] = sys[p->y_off + x];
   *energy = sys[p->energy_off];
   return DBA_OK;
 }
@@ -1697,8 +1789,12 @@ int dba_debug_trial(dba_plan* p, const dba_options* o, const dba_buffers* b, dou
   Readback rb;
   if ((s = read_flags(c, 1, rb))) return s;
   if (rb.status[0]) return DBA_ESOLVER;
-  if (delta && p->n_red > 0)
-    DBA_CUDA(cudaMemcpy(delta, c.at<double>(p->L.delta), sizeof(double) * p->n_red, cudaMemcpyDeviceToHost));
+  if (delta && p->n_red > 0) {  // natural free-pose order
+    std::vector<double> dl(p->n_red);
+    DBA_CUDA(cudaMemcpy(dl.data(), c.at<double>(p->L.delta), sizeof(double) * p->n_red, cudaMemcpyDeviceToHost));
+    for (int x = 0; x < p->n_red; ++x)
+      delta[x < 6 * p->nb ? 6 * p->natural_of_block[x / 6] + x % 6 : x] = dl[x];
+  }
   if (poses_n)
     DBA_CUDA(cudaMemcpy(poses_n, c.at<double>(p->L.poses[1]), sizeof(double) * 7 * p->N, cudaMemcpyDeviceToHost));
   if (disps_n) {  // the float64 trial state, rounded once at the boundary

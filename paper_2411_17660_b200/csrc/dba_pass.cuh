@@ -14,9 +14,9 @@
 //       energy; per-edge H_jj / g_j accumulated in registers of the warp that owns the
 //       units (two edge slots per warp, reduced once per segment); E_e,p -> the
 //       column-major shared matrix U[6e..6e+5][p]; per-edge parts of C_p, g_d,p
-//   per pixel: C_p, g_d,p (+ Eq. 4 prior); V = U_ext / sqrt(C_p), U_ext = U extended by
-//       the columns [g_d,p, c_p] (c = C/d: A5 gauge; c = d (eta + alpha m): scalefix)
-//   phase C (K3a): M_ext += V V^T over the tile's pixels on the FP64 TENSOR CORES
+//   per pixel: C_p, g_d,p (+ Eq. 4 prior), 1/C_p; U_ext = U extended by the columns
+//       [g_d,p, c_p] (c = C/d: A5 gauge; c = d (eta + alpha m): scalefix)
+//   phase C (K3a): M_ext += U_ext C^-1 U_ext^T over the tile's pixels on the FP64 TENSOR CORES
 //       (mma.sync m8n8k4 f64, DMMA): the upper triangle of M_ext in 8x8 blocks, a
 //       fixed block list per warp, accumulators in registers for the whole segment.
 //       The extra columns give, in the same product, w = E C^-1 g_d (Schur rhs) and the
@@ -131,17 +131,18 @@ __device__ __forceinline__ void pass_units(int k, int slices, int w, int& u0, in
 }
 
 struct PassSmem {
-  size_t fbuf, U, parts, dcs, dns, qc, qn, ebuf, ethb, red, emap, sflow, sl, sb, total;
+  size_t fbuf, U, parts, dcs, dns, icv, qc, qn, ebuf, ethb, red, emap, sflow, sl, sb, total;
 };
 __host__ __device__ inline PassSmem pass_smem_layout(int kmax, bool calib, int sub) {
   PassSmem s;
   size_t o = 0;
   const int nparts = calib ? 6 : 2;  // phase B: C, gd (+ E_theta x4)
   s.fbuf = o; o += sizeof(float4) * (size_t)kmax * sub;
-  s.U = o; o += sizeof(double) * (size_t)pass_mpad(kmax, calib) * pass_ustride(sub);
+  s.U = o; o += 2 * sizeof(double) * (size_t)pass_mpad(kmax, calib) * pass_ustride(sub);  // tile ring
   s.parts = o; o += sizeof(double) * (size_t)nparts * kmax * sub;
   s.dcs = o; o += sizeof(double) * sub;
   s.dns = o; o += sizeof(double) * sub;
+  s.icv = o; o += 2 * sizeof(double) * sub;
   s.qc = o; o += sizeof(double2) * sub;
   s.qn = o; o += sizeof(double2) * sub;
   s.ebuf = o; o += sizeof(double) * kPassWarps * kEdgeSlots * 32;
@@ -216,10 +217,14 @@ __global__ void __launch_bounds__(kPassThreads, 1) pass_kernel(const PassArgs A)
   const int SUB = A.sub, SL = SUB / kSlice, US = pass_ustride(SUB);
   const PassSmem L = pass_smem_layout(A.kmax, CALIB, SUB);
   float4* fbuf = reinterpret_cast<float4*>(smem + L.fbuf);  // [k][SUB] flow records
-  double* U = reinterpret_cast<double*>(smem + L.U);         // [mpad][US] column-major
+  // two column-major [mpad][US] buffers: phase B of tile t fills one while the tensor-core
+  // product of tile t-1 drains the other (DMMA and DFMA are separate pipes on B200)
+  double* const Ubuf = reinterpret_cast<double*>(smem + L.U);
+  const int ulen = pass_mpad(A.kmax, CALIB) * US;
   double* parts = reinterpret_cast<double*>(smem + L.parts);
   double* dcs = reinterpret_cast<double*>(smem + L.dcs);
   double* dns = reinterpret_cast<double*>(smem + L.dns);
+  double* const icvb = reinterpret_cast<double*>(smem + L.icv);  // 1 / C_p, per tile buffer
   double2* qcs = reinterpret_cast<double2*>(smem + L.qc);  // normalised pixel rays at x_c
   double2* qns = reinterpret_cast<double2*>(smem + L.qn);  // ... at x_n
   double* ebuf = reinterpret_cast<double*>(smem + L.ebuf);
@@ -268,14 +273,17 @@ __global__ void __launch_bounds__(kPassThreads, 1) pass_kernel(const PassArgs A)
       if (CALIB) ethb[x] = 0.0;
     }
     // padding columns of U (mext..mpad) stay zero for the whole segment
-    for (int x = tid; x < (mpad - mext) * SUB; x += kPassThreads) U[(mext + x / SUB) * US + x % SUB] = 0.0;
+    for (int x = tid; x < 2 * (mpad - mext) * SUB; x += kPassThreads) {
+      const int y = x % ((mpad - mext) * SUB);
+      Ubuf[(x >= (mpad - mext) * SUB ? ulen : 0) + (mext + y / SUB) * US + y % SUB] = 0.0;
+    }
     // tensor-core blocks of this warp: row-major enumeration of the upper triangle of
     // (mpad/8)^2 blocks, contiguous chunks (a warp's blocks mostly share their row)
     const int nb8 = mpad >> 3, nblk = nb8 * (nb8 + 1) / 2;
     const int per = (nblk + kPassWarps - 1) / kPassWarps;
     const int bq0 = min(warp * per, nblk), nmine = min(per, nblk - bq0);
     int offA[MB], offB[MB];
-    unsigned reuseA = 0, diag = 0;  // per block: A fragment = the previous block's / B = A
+    unsigned reuseA = 0;  // per block: A fragment = the previous block's
     {
       int bi = 0, rowlen = nb8, b = nmine > 0 ? bq0 : 0;  // idle warps: any valid block
       while (b >= rowlen) {
@@ -289,7 +297,6 @@ __global__ void __launch_bounds__(kPassThreads, 1) pass_kernel(const PassArgs A)
         offA[q] = (8 * bi + (lane >> 2)) * US + (lane & 3);
         offB[q] = (8 * bj + (lane >> 2)) * US + (lane & 3);
         if (q > 0 && offA[q] == offA[q - 1]) reuseA |= 1u << q;
-        if (bi == bj) diag |= 1u << q;
         if (++bj == nb8) {
           ++bi;
           bj = bi;
@@ -322,6 +329,45 @@ __global__ void __launch_bounds__(kPassThreads, 1) pass_kernel(const PassArgs A)
       kappa = (gs[1] - hd) / gs[0];
     }
 
+    // M_ext += U C^-1 U^T over k-steps [ks0, ks1) of one tile buffer: a warp's blocks, 4
+    // pixels per step, A = U / C (each lane scales by its pixel's 1/C_p), B = U
+    auto gemm = [&](const double* Ub, const double* ic_b, int ks0, int ks1) {
+      if (nmine == MB) {
+        // the common case: every block slot used, so the k-loop has no predication
+        // (no per-MMA warp re-convergence), and A fragments shared by consecutive blocks
+        // of one row are loaded and scaled once
+        for (int ks = ks0; ks < ks1; ++ks) {
+          const int p0 = 4 * ks;
+          const double ic = ic_b[p0 + (lane & 3)];
+          double av[MB], bv[MB];
+#pragma unroll
+          for (int q = 0; q < MB; ++q) {
+            if ((reuseA >> q) & 1u)
+              av[q] = av[q > 0 ? q - 1 : 0];
+            else
+              av[q] = Ub[offA[q] + p0] * ic;
+            bv[q] = Ub[offB[q] + p0];
+          }
+#pragma unroll
+          for (int q = 0; q < MB; ++q) dmma884(macc[q], av[q], bv[q]);
+        }
+      } else if (nmine > 0) {
+        for (int ks = ks0; ks < ks1; ++ks) {
+          const int p0 = 4 * ks;
+          const double ic = ic_b[p0 + (lane & 3)];
+#pragma unroll
+          for (int q = 0; q < MB; ++q) {
+            if (q < nmine) {
+              const double av = Ub[offA[q] + p0] * ic;
+              const double bv = Ub[offB[q] + p0];
+              dmma884(macc[q], av, bv);
+            }
+          }
+        }
+      }
+    };
+    const int nks = SUB / 4;
+
     // cp.async staging of a tile's flow records (16 B each) and disparities;
     // out-of-range pixels are zero-filled
     auto prefetch = [&](int tile) {
@@ -345,6 +391,12 @@ __global__ void __launch_bounds__(kPassThreads, 1) pass_kernel(const PassArgs A)
 
     for (int tile = A.seg_t0[sg]; tile < A.seg_t1[sg]; ++tile) {
       const int pbase = tile * SUB;
+      const int tb = (tile - A.seg_t0[sg]) & 1;
+      double* const U = Ubuf + tb * ulen;  // this tile's buffer
+      double* const icv = icvb + tb * SUB;
+      const bool drain = tile > A.seg_t0[sg];  // the previous tile's product is pending
+      const double* const Up = Ubuf + (tb ^ 1) * ulen;
+      const double* const icp = icvb + (tb ^ 1) * SUB;
       asm volatile("cp.async.wait_all;" ::: "memory");
       for (int x = tid; x < SUB; x += kPassThreads) {
         const int p = pbase + x;
@@ -421,7 +473,16 @@ __global__ void __launch_bounds__(kPassThreads, 1) pass_kernel(const PassArgs A)
       }
       __syncthreads();
       // ------------------------------------------------------------ phase B
+      // the previous tile's tensor-core k-steps are spread over this warp's units: the
+      // DMMAs issue between the float64 geometry and drain in the background
+      const int kper = u1 > u0 ? (nks + (u1 - u0) - 1) / (u1 - u0) : 0;
+      int ksd = 0;
       for (int u = u0; u < u1; ++u) {
+        if (drain) {
+          const int ks1 = min(ksd + kper, nks);
+          gemm(Up, icp, ksd, ks1);
+          ksd = ks1;
+        }
         const int a = u / SL, slot = a - e0;
         const int pl = (u - a * SL) * kSlice + lane, p = pbase + pl;
         const bool in = p < P;
@@ -512,12 +573,13 @@ __global__ void __launch_bounds__(kPassThreads, 1) pass_kernel(const PassArgs A)
           ethb[(warp * kEdgeSlots + slot) * 32 + lane] += rs;
         }
       }
+      if (drain) gemm(Up, icp, ksd, nks);  // warps without units (or a remainder)
       __syncthreads();
       if (tile + 1 < A.seg_t1[sg]) prefetch(tile + 1);  // overlaps the rest of the tile
       // ------------------------------------------------------------ per pixel
-      // threads per pixel: all form C_p, g_d,p; each scales a share of the columns
-      {
-        const int tpp = kPassThreads / SUB, pl = tid % SUB, part = tid / SUB;
+      // C_p, g_d,p (+ Eq. 4 prior), 1/C_p and the extra columns; the 1/C_p scaling is
+      // applied to the A fragments of the product (M_ext = sum_p U_p U_p^T / C_p)
+      for (int pl = tid; pl < SUB; pl += kPassThreads) {
         const int p = pbase + pl;
         const bool in = p < P;
         double C = A.eta, gd = 0.0;
@@ -533,72 +595,31 @@ __global__ void __launch_bounds__(kPassThreads, 1) pass_kernel(const PassArgs A)
           const double dd = (double)A.prior[fp] - dn;
           C += ap;
           gd += ap * dd;
-          if (part == 0) {
-            facc[0] += ap * dd * dd;
-            fpri = fma(dn * ap, dd, fpri);
-          }
+          facc[0] += ap * dd * dd;
+          fpri = fma(dn * ap, dd, fpri);
         }
-        // V = U_ext / sqrt(C): the product below is then M_ext = V V^T
-        const double sq = (in && !A.freeze) ? rsqrt(C) : 0.0;  // frozen d: no fill-in
-        const int ne = 6 * k;
-        const int c0 = (ne * part) / tpp, c1 = (ne * (part + 1)) / tpp;
-        for (int c = c0; c < c1; ++c) U[c * US + pl] *= sq;
-        if (part == tpp - 1) {
-          if (CALIB) {
-            double Et[4] = {0.0, 0.0, 0.0, 0.0};
-            for (int a = 0; a < k; ++a)
+        icv[pl] = (in && !A.freeze) ? __drcp_rn(C) : 0.0;  // frozen d: no fill-in
+        if (CALIB) {
+          double Et[4] = {0.0, 0.0, 0.0, 0.0};
+          for (int a = 0; a < k; ++a)
 #pragma unroll
-              for (int r = 0; r < 4; ++r) Et[r] += Pth[(r * KM + a) * SUB + pl];
+            for (int r = 0; r < 4; ++r) Et[r] += Pth[(r * KM + a) * SUB + pl];
 #pragma unroll
-            for (int r = 0; r < 4; ++r) U[(ne + r) * US + pl] = Et[r] * sq;
-          }
-          // second extra column: A5 gauge c = C/d, or (scalefix) c = d (eta + alpha m), whose
-          // E C^-1 c is the reduced system's exact row along the monocular scale direction
-          const double cx = A.scalefix ? dn * (A.eta + ap) : C / dn;
-          U[mu * US + pl] = gd * sq;
-          U[(mu + 1) * US + pl] = in ? cx * sq : 0.0;
+          for (int r = 0; r < 4; ++r) U[(6 * k + r) * US + pl] = Et[r];
         }
+        // second extra column: A5 gauge c = C/d, or (scalefix) c = d (eta + alpha m), whose
+        // E C^-1 c is the reduced system's exact row along the monocular scale direction
+        const double cx = A.scalefix ? dn * (A.eta + ap) : C / dn;
+        U[mu * US + pl] = gd;
+        U[(mu + 1) * US + pl] = in ? cx : 0.0;
       }
       __syncthreads();
-      // ------------------------------------------------------------ phase C (K3a)
-      // M_ext += V V^T: a warp's blocks, k-steps of 4 pixels, fragments straight from U
-      if (nmine == MB) {
-        // the common case: every block slot used, so the k-loop has no predication
-        // (no per-MMA warp re-convergence) and A fragments shared by consecutive blocks
-        // of one row, and B = A on diagonal blocks, are loaded once
-        for (int p0 = 0; p0 < SUB; p0 += 32) {
-#pragma unroll
-          for (int kk = 0; kk < 32; kk += 4) {
-            double av[MB], bv[MB];
-#pragma unroll
-            for (int q = 0; q < MB; ++q) {
-              if ((reuseA >> q) & 1u)
-                av[q] = av[q > 0 ? q - 1 : 0];
-              else
-                av[q] = U[offA[q] + p0 + kk];
-              if ((diag >> q) & 1u)
-                bv[q] = av[q];
-              else
-                bv[q] = U[offB[q] + p0 + kk];
-            }
-#pragma unroll
-            for (int q = 0; q < MB; ++q) dmma884(macc[q], av[q], bv[q]);
-          }
-        }
-      } else if (nmine > 0) {
-#pragma unroll 2
-        for (int p0 = 0; p0 < SUB; p0 += 4) {
-#pragma unroll
-          for (int q = 0; q < MB; ++q) {
-            if (q < nmine) {
-              const double av = U[offA[q] + p0];
-              const double bv = U[offB[q] + p0];
-              dmma884(macc[q], av, bv);
-            }
-          }
-        }
-      }
-      __syncthreads();
+      // (phase C of this tile runs interleaved with the next tile's phase B)
+    }
+    __syncthreads();  // the last tile's 1/C_p and extra columns
+    {  // ------------------------------------------------------------ phase C, last tile
+      const int tb = (A.seg_t1[sg] - 1 - A.seg_t0[sg]) & 1;
+      gemm(Ubuf + tb * ulen, icvb + tb * SUB, 0, nks);
     }
 
     // ------------------------------------------------------------ segment outputs

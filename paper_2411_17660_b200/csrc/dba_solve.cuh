@@ -43,6 +43,7 @@ constexpr int kStageWarp = 3;       // also a trailing warp; issues the next row
 constexpr int kTrailThreads = 224;  // warps 0..6
 constexpr int kMaxBand = 24;        // compiled limit on BW
 constexpr int kRing = 32;           // backward-sweep factor-row ring depth (hides the bulk-copy latency)
+constexpr int kRingWide = 8;        // ... for wide bands (a folded loop closure): 8 rows of BW blocks
 // blocks of the shared-memory window are kWB doubles apart (36 + 2 padding): block
 // starts then fall on 8 different bank offsets instead of 4, which removes most of
 // the bank conflicts of the trailing update (measured 1.5k -> 1.2k cycles per pivot)
@@ -109,11 +110,11 @@ __host__ __device__ inline long long solve_mid_len(int BW) {
 struct SolveSmem {
   size_t win, ring, th, thL, z, thm, thLm, zm, dinv, pbuf, cbuf, tbuf, pairs, xo, bars, total;
 };
-__host__ __device__ inline SolveSmem solve_smem_layout(int nb, int BW, int calib) {
+__host__ __device__ inline SolveSmem solve_smem_layout(int nb, int BW, int calib, int ring = kRing) {
   SolveSmem s;
   size_t o = 0;
   s.win = o; o += sizeof(double) * (size_t)(BW + 1) * (BW + 1) * kWB;
-  s.ring = o; o += sizeof(double) * (size_t)kRing * BW * 36;  // backward sweep: L blocks of kRing rows
+  s.ring = o; o += sizeof(double) * (size_t)ring * BW * 36;  // backward sweep: L blocks of `ring` rows
   s.th = o; o += sizeof(double) * (calib ? (size_t)nb * 24 + 16 : 0);
   s.thL = o; o += sizeof(double) * (calib ? (size_t)nb * 24 : 0);
   s.z = o; o += sizeof(double) * ((size_t)6 * nb + 4);
@@ -127,7 +128,7 @@ __host__ __device__ inline SolveSmem solve_smem_layout(int nb, int BW, int calib
   s.pairs = o; o += sizeof(short2) * (size_t)(BW * (BW + 1) / 2 + 1);
   o = (o + 7) & ~size_t(7);
   s.xo = o; o += sizeof(double) * ((size_t)6 * nb + 4);  // refinement: the unrefined step
-  s.bars = o; o += sizeof(unsigned long long) * 2 * kRing;  // backward-sweep ring full/empty mbarriers
+  s.bars = o; o += sizeof(unsigned long long) * 2 * ring;  // backward-sweep ring full/empty mbarriers
   s.total = (o + 15) & ~size_t(15);
   return s;
 }
@@ -534,7 +535,7 @@ __device__ inline bool theta_solve(const double* T, double* zt, double lam, doub
 // b < npiv.  On entry z[0, npiv) holds the forward rhs and z[npiv, nrows) the already
 // known x of the rows that were not pivoted; xt (4) the theta solution (calib).
 // `ring` (>= 8 factor rows) streams Lband rows via cp.async; tmp (6 npiv) staging.
-template <int NS>
+template <int NS, int RD>
 __device__ inline void chain_backward(double* z, const double* thL, const double* xt, const double* Lband,
                                       double* ring, unsigned long long* bars, int nrows, int npiv, int BW, int calib,
                                       double* tmp) {
@@ -558,7 +559,6 @@ __device__ inline void chain_backward(double* z, const double* thL, const double
   // stream through a ring of RD slots: the staging warp refills a slot with one bulk
   // async copy (TMA engine) once the sweep warp has released it (full/empty mbarrier
   // pairs), so the sweep's critical path holds no copy issue and no proxy fence.
-  constexpr int RD = kRing;
   const unsigned full0 = (unsigned)__cvta_generic_to_shared(bars), empty0 = full0 + 8 * RD;
   const unsigned bytes = (unsigned)(BW * 36 * sizeof(double));
   if (tid == 0)
@@ -578,7 +578,7 @@ __device__ inline void chain_backward(double* z, const double* thL, const double
           : "memory");
   };
   if (warp == kStageWarp && lane == 0 && nrows > 1 && !DBA_NOPRODUCER) {
-    static_assert(RD == 32, "four batches of 8 slots");
+    static_assert(RD % 8 == 0 && RD <= 32, "batches of 8 slots, at most four");
     unsigned fills = 0;  // 8 bits per batch of 8 slots: how often the batch was entered
     for (int i = 0; nrows - 1 - i >= 1; ++i) {
       const int a = nrows - 1 - i, slot = a % RD, batch = slot / 8;
@@ -877,14 +877,14 @@ __device__ void scale_correct(const SolveArgs& A, double lam) {
 }
 
 // one-sided solve (small systems)
-template <int NS>
+template <int NS, int RD>
 __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const SolveArgs A0) {
   pdl_enter();
   if (A0.status[3] != 0) return;  // GN loop finished
   double lam;
   const SolveArgs A = spec_view(A0, blockIdx.x, lam);
   extern __shared__ __align__(16) unsigned char smem[];
-  const SolveSmem L = solve_smem_layout(A.nb, A.BW, A.calib);
+  const SolveSmem L = solve_smem_layout(A.nb, A.BW, A.calib, RD);
   __shared__ int fail;
   const int tid = threadIdx.x;
   const int nb = A.nb, BW = A.BW, NR = (BW + 1) * 36;
@@ -906,7 +906,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const SolveArgs
     if (tid == 0) A.status[0] = 1;
     return;
   }
-  chain_backward<NS>(S.z, S.thL, S.z + 6 * nb, A.Lband, S.ring, S.bars, nb, nb, BW, A.calib, A.delta);
+  chain_backward<NS, RD>(S.z, S.thL, S.z + 6 * nb, A.Lband, S.ring, S.bars, nb, nb, BW, A.calib, A.delta);
   for (int x = tid; x < 6 * nb + (A.calib ? 4 : 0); x += kSolveThreads) A.delta[x] = S.z[x];
   if (A.refine) {
     double* xo = reinterpret_cast<double*>(smem + L.xo);
@@ -928,7 +928,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const SolveArgs
       }
       __syncthreads();
     }
-    chain_backward<NS>(S.z, S.thL, S.z + 6 * nb, A.Lband, S.ring, S.bars, nb, nb, BW, A.calib, A.delta);
+    chain_backward<NS, RD>(S.z, S.thL, S.z + 6 * nb, A.Lband, S.ring, S.bars, nb, nb, BW, A.calib, A.delta);
     for (int x = tid; x < n; x += kSolveThreads) A.delta[x] = xo[x] + S.z[x];
   }
   if (A.scalefix) {
@@ -938,7 +938,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const SolveArgs
 }
 
 // two-sided solve: 2 cooperative CTAs (see the header comment)
-template <int NS>
+template <int NS, int RD>
 __global__ void __launch_bounds__(kSolveThreads, 1) solve2_kernel(const SolveArgs A0) {
   pdl_enter();
   namespace cg = cooperative_groups;
@@ -947,7 +947,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve2_kernel(const SolveArg
   double lam;
   const SolveArgs A = spec_view(A0, blockIdx.x >> 1, lam);  // CTA pair per candidate
   extern __shared__ __align__(16) unsigned char smem[];
-  const SolveSmem L = solve_smem_layout(A.nb, A.BW, A.calib);
+  const SolveSmem L = solve_smem_layout(A.nb, A.BW, A.calib, RD);
   __shared__ int fail;
   __shared__ double xts[4];
   const int tid = threadIdx.x, cta = blockIdx.x & 1;
@@ -1049,7 +1049,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve2_kernel(const SolveArg
     if (calib && tid == 0 && !fail)
       if (!theta_solve(M.th + (size_t)BW * 24, M.z + 6 * BW, lam, A.cond)) fail = 1;
     __syncthreads();
-    if (!fail) chain_backward<NS>(M.z, M.thL, M.z + 6 * BW, Lm, M.ring, M.bars, BW, BW, BWm, calib, A.delta);
+    if (!fail) chain_backward<NS, RD>(M.z, M.thL, M.z + 6 * BW, Lm, M.ring, M.bars, BW, BW, BWm, calib, A.delta);
     for (int x = tid; x < 6 * BW + (calib ? 4 : 0); x += kSolveThreads) xsol[x] = M.z[x];
     __syncthreads();
     if (tid == 0 && fail) atomicExch(gfail, 1);
@@ -1072,7 +1072,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve2_kernel(const SolveArg
   if (tid < 4) xts[tid] = calib ? xsol[6 * BW + tid] : 0.0;
   __syncthreads();
   double* tmp = A.delta + (cta == 0 ? 0 : 6 * (m + BW));  // staging inside this chain's output range
-  chain_backward<NS>(S.z, S.thL, xts, Lb, S.ring, S.bars, nrows, npiv, BW, calib, tmp);
+  chain_backward<NS, RD>(S.z, S.thL, xts, Lb, S.ring, S.bars, nrows, npiv, BW, calib, tmp);
   for (int x = tid; x < 6 * npiv; x += kSolveThreads) {
     const int a = x / 6, s = x % 6;
     A.delta[6 * (cta == 0 ? a : nb - 1 - a) + s] = S.z[x];
@@ -1136,7 +1136,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve2_kernel(const SolveArg
         }
         __syncthreads();
       }
-      chain_backward<NS>(M.z, M.thL, M.z + 6 * BW, Lm, M.ring, M.bars, BW, BW, BW - 1, calib, A.delta + 6 * m);
+      chain_backward<NS, RD>(M.z, M.thL, M.z + 6 * BW, Lm, M.ring, M.bars, BW, BW, BW - 1, calib, A.delta + 6 * m);
       for (int x = tid; x < 6 * BW + (calib ? 4 : 0); x += kSolveThreads) xsol[x] = M.z[x];
     }
     __threadfence();
@@ -1149,7 +1149,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve2_kernel(const SolveArg
       if (tid < 4) xts[tid] = calib ? xsol[6 * BW + tid] : 0.0;
       __syncthreads();
       double* tmp = A.delta + (cta == 0 ? 0 : 6 * (m + BW));
-      chain_backward<NS>(S.z, S.thL, xts, Lb, S.ring, S.bars, nrows, npiv, BW, calib, tmp);
+      chain_backward<NS, RD>(S.z, S.thL, xts, Lb, S.ring, S.bars, nrows, npiv, BW, calib, tmp);
       for (int x = tid; x < 6 * npiv; x += kSolveThreads) {
         const int a = x / 6, s2 = x % 6;
         const int g = 6 * (cta == 0 ? a : nb - 1 - a) + s2;
