@@ -316,7 +316,8 @@ int dba_plan_create(const dba_problem_desc* d, dba_plan** out) {
   }
 
   // ---- reduced variables: free poses, theta last.  The block order is the natural one
-  // unless a reverse Cuthill-McKee order of the fill-in graph gives a narrower band: a
+  // unless the fold of a ring or a reverse Cuthill-McKee order of the fill-in graph gives
+  // a narrower band: a
   // loop-closure edge (e.g. 0 <-> 299 on a 300-frame chain) makes the natural band span
   // the whole chain, while RCM folds the cycle (band 20 blocks instead of 298).
   std::vector<std::vector<int>> vars(N);  // each source frame's local variables
@@ -375,6 +376,32 @@ int dba_plan_create(const dba_problem_desc* d, dba_plan** out) {
         starts.push_back(k);
         break;
       }
+    auto try_order = [&](const std::vector<int>& order) {  // order: free poses, new block order
+      std::vector<int> ridx(N, -1);
+      for (size_t i = 0; i < order.size(); ++i) ridx[order[i]] = (int)i;
+      const int B2 = band_of(ridx);
+      if (B2 < BW) {
+        BW = B2;
+        std::vector<int> nat(N, -1);
+        int c2 = 0;
+        for (int k = 0; k < N; ++k)
+          if (!d->fixed[k]) nat[k] = c2++;
+        p->fixed_ridx = ridx;
+        for (int k = 0; k < N; ++k)
+          if (ridx[k] >= 0) p->natural_of_block[ridx[k]] = nat[k];
+      }
+    };
+    {  // the fold of a ring: first, last, second, second-to-last, ... (a closed orbit)
+      std::vector<int> nat_order;
+      for (int k = 0; k < N; ++k)
+        if (!d->fixed[k]) nat_order.push_back(k);
+      std::vector<int> fold;
+      for (int lo = 0, hi = (int)nat_order.size() - 1; lo <= hi; ++lo, --hi) {
+        fold.push_back(nat_order[lo]);
+        if (hi != lo) fold.push_back(nat_order[hi]);
+      }
+      try_order(fold);
+    }
     for (int s0 : starts) {
       std::vector<char> seen(N, 0);
       std::vector<int> order;
@@ -396,19 +423,8 @@ int dba_plan_create(const dba_problem_desc* d, dba_plan** out) {
       bfs(s0);
       for (int k : free_sorted)
         if (!seen[k]) bfs(k);
-      std::vector<int> ridx(N, -1);
-      for (size_t i = 0; i < order.size(); ++i) ridx[order[order.size() - 1 - i]] = (int)i;
-      const int B2 = band_of(ridx);
-      if (B2 < BW) {
-        BW = B2;
-        std::vector<int> nat(N, -1);
-        int c2 = 0;
-        for (int k = 0; k < N; ++k)
-          if (!d->fixed[k]) nat[k] = c2++;
-        p->fixed_ridx = ridx;
-        for (int k = 0; k < N; ++k)
-          if (ridx[k] >= 0) p->natural_of_block[ridx[k]] = nat[k];
-      }
+      std::reverse(order.begin(), order.end());  // reverse Cuthill-McKee
+      try_order(order);
     }
   }
   p->nb = nfree;

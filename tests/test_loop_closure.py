@@ -115,9 +115,8 @@ def test_backend_graph_with_loops_solves():
     poses0, disps0 = scenes.perturbed_state(sc, fr)
     true_p = np.stack([sc.w2c[k] for k in fr])
     true_d = np.stack([sc.disparity(k) for k in fr]).astype(np.float32)
-    edges = graph.build_backend_graph(true_p, true_d, sc.intr, fr, loops=[(0, n - 1)])
-    ii = np.array([a for a, b in edges], np.int32)
-    jj = np.array([b for a, b in edges], np.int32)
+    ii, jj = graph.build_backend_graph(true_p, true_d, sc.intr, fr, loops=[(0, n - 1)])
+    edges = list(zip(ii.tolist(), jj.tolist()))
     assert (0, n - 1) in edges and len(edges) <= 1500
     flow = np.stack([sc.flow_record(int(a), int(b)) for a, b in zip(ii, jj)])
     fixed = np.zeros(n, bool)
