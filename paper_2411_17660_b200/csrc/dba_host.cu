@@ -98,7 +98,7 @@ struct dba_plan {
   int calib = 0, prior = 0, freeze_d = 0, gauge_on = 0, gauge_frame = -1, rank = 0, nranks = 1;
   int scalefix = 0, anchor = -1;  // prior-fixed monocular scale: exact-row step correction
   int f0 = 0, f1 = 0, NL = 0, EL = 0, kmax = 0, nb = 0, BW = 0, n_red = 0;
-  int n_tiles = 0, G = 0, nseg = 0, n_units = 0, nve = kEdgeVals, sub = 128, mb = 6, ring = 32;
+  int n_tiles = 0, G = 0, nseg = 0, n_units = 0, nve = kEdgeVals, sub = 128, mb = 2, ring = 32;
   size_t pass_smem = 0, solve_smem = 0;
   long long sys_len = 0;  // doubles in one packed reduced system
   long long spec_delta = 0, spec_Lband = 0, spec_rLband = 0, spec_mid = 0;  // per damping candidate
@@ -474,9 +474,11 @@ int dba_plan_create(const dba_problem_desc* d, dba_plan** out) {
       p->sub = 64;
     }
     p->pass_smem = s.total;
-    const int mb = pass_mb(pass_mpad(std::max(p->kmax, 1), p->calib));
-    p->mb = mb <= 5 ? 5 : mb <= 6 ? 6 : 12;  // 5: radius-5 graphs (k = 10); 6: with intrinsics
-    if (p->pass_smem > 225 * 1024 || mb > 12) {
+    // quads per warp of the tensor-core product (pass_quads): 2 up to 80 GEMM rows
+    // (radius-5 graphs, with or without intrinsics), 4 up to 112 (out-degree 16)
+    const int qm = pass_qmax(pass_mpad(std::max(p->kmax, 1), p->calib) >> 4);
+    p->mb = qm <= 2 ? 2 : 4;
+    if (p->pass_smem > 225 * 1024 || qm > 4) {
       delete p;
       return DBA_ECAPACITY;
     }
@@ -1031,9 +1033,9 @@ int launch_prep(Ctx& c, int cur, int nxt, bool init, int cand = 0) {
   return DBA_OK;
 }
 
-template <bool CALIB, int MB>
+template <bool CALIB, int QMAX>
 int launch_pass_t(Ctx& c, const PassArgs& a) {
-  auto k = pass_kernel<CALIB, MB>;
+  auto k = c.p->sub == 128 ? pass_kernel<CALIB, QMAX, 128> : pass_kernel<CALIB, QMAX, 64>;
   DBA_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.p->pass_smem));
   auto& pr = c.p->prof;
   std::pair<int, int> ev{-1, -1};
@@ -1099,11 +1101,8 @@ int launch_pass(Ctx& c, int cur, int nxt, bool backsub, bool system, bool gated 
   a.seg_off_edge = c.at<long long>(p->L.seg_off_edge);
   a.seg_off_M = c.at<long long>(p->L.seg_off_M);
   a.seg_off_w = c.at<long long>(p->L.seg_off_w);
-  if (p->calib)
-    return p->mb == 5 ? launch_pass_t<true, 5>(c, a) : p->mb == 6 ? launch_pass_t<true, 6>(c, a)
-                                                             : launch_pass_t<true, 12>(c, a);
-  return p->mb == 5 ? launch_pass_t<false, 5>(c, a) : p->mb == 6 ? launch_pass_t<false, 6>(c, a)
-                                                            : launch_pass_t<false, 12>(c, a);
+  if (p->calib) return p->mb == 2 ? launch_pass_t<true, 2>(c, a) : launch_pass_t<true, 4>(c, a);
+  return p->mb == 2 ? launch_pass_t<false, 2>(c, a) : launch_pass_t<false, 4>(c, a);
 }
 
 // LM controller inputs: the trial (slot 1) energy, the flags word and the options

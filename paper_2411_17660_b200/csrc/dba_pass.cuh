@@ -103,16 +103,54 @@ __device__ __forceinline__ T transpose_reduce32(T (&v)[32], int lane) {
 }
 
 __host__ __device__ inline int pass_mu(int k, bool calib) { return 6 * k + (calib ? 4 : 0); }
-// GEMM rows: U (mu) + [g_d, c], padded to the 8x8 tensor-core block
+// GEMM rows: U (mu) + [g_d, c], padded to pairs of 8x8 tensor-core blocks
 __host__ __device__ inline int pass_mext(int k, bool calib) { return pass_mu(k, calib) + 2; }
-__host__ __device__ inline int pass_mpad(int k, bool calib) { return (pass_mext(k, calib) + 7) & ~7; }
+__host__ __device__ inline int pass_mpad(int k, bool calib) { return (pass_mext(k, calib) + 15) & ~15; }
 // column stride of the column-major U (doubles): = 4 (mod 16) makes both the phase-B
-// stores (a lane per pixel) and the m8n8k4 fragment loads (4 pixels x 8 columns per
+// stores (a lane per pixel) and the m8n8k4 fragment loads (4 pixels x 8 rows per
 // half-warp pair) bank-conflict free
-__host__ __device__ inline int pass_ustride(int sub) { return sub + 4; }
-__host__ __device__ inline int pass_nblk(int mpad) { return (mpad / 8) * (mpad / 8 + 1) / 2; }
-// blocks of M_ext per warp (register accumulators, 2 doubles each)
-__host__ __device__ inline int pass_mb(int mpad) { return (pass_nblk(mpad) + kPassWarps - 1) / kPassWarps; }
+__host__ __device__ constexpr int pass_ustride(int sub) { return sub + 4; }
+
+// Work split of the symmetric product M_ext = V C^-1 V^T (upper triangle, 8x8 blocks).
+// The np = mpad/16 row PAIRS of blocks form quads: a cross quad (r < c) is the 2x2 block
+// square {2r, 2r+1} x {2c, 2c+1} (4 fragments loaded, 4 DMMAs per k-step), a diagonal
+// quad (r = c) the blocks (2r,2r), (2r,2r+1), (2r+1,2r+1) (2 fragments: A and B
+// fragments of one block row are the same shared-memory words, 3 DMMAs).  Quads go to
+// the 8 warps longest-first (cross, then diagonal) onto the least-loaded warp, lowest
+// index on ties; every thread evaluates the same deterministic assignment.
+// Returns the number of quads of warp `w`, their pairs in (qr, qc) when non-null.
+template <int QMAX>
+__host__ __device__ inline int pass_quads(int np, int w, int* qr, int* qc) {
+  int load[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  int n = 0;
+  for (int pass = 0; pass < 2; ++pass)
+    for (int r = 0; r < np; ++r)
+      for (int c = r; c < np; ++c) {
+        if ((pass == 0) != (r < c)) continue;
+        int best = 0;
+        for (int x = 1; x < 8; ++x)
+          if (load[x] < load[best]) best = x;
+        load[best] += r < c ? 4 : 3;
+        if (best == w) {
+          if (qr) {
+#pragma unroll
+            for (int s = 0; s < QMAX; ++s)  // compile-time register index
+              if (s == n) {
+                qr[s] = r;
+                qc[s] = c;
+              }
+          }
+          ++n;
+        }
+      }
+  return n;
+}
+// largest per-warp quad count for np row pairs (the plan picks QMAX from it)
+__host__ __device__ inline int pass_qmax(int np) {
+  int m = 0;
+  for (int w = 0; w < 8; ++w) m = pass_quads<1>(np, w, nullptr, nullptr) > m ? pass_quads<1>(np, w, nullptr, nullptr) : m;
+  return m;
+}
 
 // phase-B unit range of warp w: contiguous, at most kEdgeSlots distinct edges
 __device__ __forceinline__ void pass_units(int k, int slices, int w, int& u0, int& u1) {
@@ -207,14 +245,14 @@ __device__ __forceinline__ void theta_jac(const double R[9], const PixTerms& T, 
   Tv[3] = 1.0 - cv1;
 }
 
-template <bool CALIB, int MB>
+template <bool CALIB, int QMAX, int SUB>
 __global__ void __launch_bounds__(kPassThreads, 1) pass_kernel(const PassArgs A) {
   pdl_enter();
   if (trial_skipped(A.status)) return;
   if (A.runs && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(A.runs, 1ull);
   extern __shared__ __align__(16) unsigned char smem[];
   constexpr int NVE = kEdgeVals + (CALIB ? kCalibVals : 0);
-  const int SUB = A.sub, SL = SUB / kSlice, US = pass_ustride(SUB);
+  constexpr int SL = SUB / kSlice, US = pass_ustride(SUB);
   const PassSmem L = pass_smem_layout(A.kmax, CALIB, SUB);
   float4* fbuf = reinterpret_cast<float4*>(smem + L.fbuf);  // [k][SUB] flow records
   // two column-major [mpad][US] buffers: phase B of tile t fills one while the tensor-core
@@ -249,7 +287,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) pass_kernel(const PassArgs A)
     const int f = A.frame_of[fl];
     const int mu = pass_mu(k, CALIB);
     const int mext = mu + 2;
-    const int mpad = (mext + 7) & ~7;
+    const int mpad = (mext + 15) & ~15;
     double* Pa0 = parts;                 // [k][SUB]  C part
     double* Pa1 = parts + KM * SUB;      // [k][SUB]  g_d part
     double* Pth = parts + 2 * KM * SUB;  // [4][k][SUB] E_theta parts (phase B, calib)
@@ -277,35 +315,26 @@ __global__ void __launch_bounds__(kPassThreads, 1) pass_kernel(const PassArgs A)
       const int y = x % ((mpad - mext) * SUB);
       Ubuf[(x >= (mpad - mext) * SUB ? ulen : 0) + (mext + y / SUB) * US + y % SUB] = 0.0;
     }
-    // tensor-core blocks of this warp: row-major enumeration of the upper triangle of
-    // (mpad/8)^2 blocks, contiguous chunks (a warp's blocks mostly share their row)
-    const int nb8 = mpad >> 3, nblk = nb8 * (nb8 + 1) / 2;
-    const int per = (nblk + kPassWarps - 1) / kPassWarps;
-    const int bq0 = min(warp * per, nblk), nmine = min(per, nblk - bq0);
-    int offA[MB], offB[MB];
-    unsigned reuseA = 0;  // per block: A fragment = the previous block's
-    {
-      int bi = 0, rowlen = nb8, b = nmine > 0 ? bq0 : 0;  // idle warps: any valid block
-      while (b >= rowlen) {
-        b -= rowlen;
-        ++bi;
-        --rowlen;
-      }
-      int bj = bi + b;
+    // tensor-core quads of this warp (pass_quads): fragment pointers into a U buffer are
+    // U + fo_r[q] (rows of block 2r; block 2r+1 is kRB doubles further) and U + fo_c[q]
+    const int np = mpad >> 4;
+    int qr[QMAX], qc[QMAX];
 #pragma unroll
-      for (int q = 0; q < MB; ++q) {
-        offA[q] = (8 * bi + (lane >> 2)) * US + (lane & 3);
-        offB[q] = (8 * bj + (lane >> 2)) * US + (lane & 3);
-        if (q > 0 && offA[q] == offA[q - 1]) reuseA |= 1u << q;
-        if (++bj == nb8) {
-          ++bi;
-          bj = bi;
-        }
-      }
+    for (int q = 0; q < QMAX; ++q) qr[q] = qc[q] = 0;
+    const int nq = pass_quads<QMAX>(np, warp, qr, qc);
+    const int lane_off = (lane >> 2) * US + (lane & 3);
+    int fo_r[QMAX], fo_c[QMAX];
+#pragma unroll
+    for (int q = 0; q < QMAX; ++q) {
+      fo_r[q] = 16 * qr[q] * US + lane_off;
+      fo_c[q] = 16 * qc[q] * US + lane_off;
     }
-    double macc[MB][2];
+    constexpr int kRB = 8 * US;  // doubles between the fragments of blocks 2r and 2r+1
+    double macc[QMAX][4][2];
 #pragma unroll
-    for (int q = 0; q < MB; ++q) macc[q][0] = macc[q][1] = 0.0;
+    for (int q = 0; q < QMAX; ++q)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) macc[q][b][0] = macc[q][b][1] = 0.0;
     double hacc[kEdgeSlots][28];  // per-edge H_jj, g_j, energy of this warp's units (whole segment)
 #pragma unroll
     for (int s = 0; s < kEdgeSlots; ++s)
@@ -329,39 +358,39 @@ __global__ void __launch_bounds__(kPassThreads, 1) pass_kernel(const PassArgs A)
       kappa = (gs[1] - hd) / gs[0];
     }
 
-    // M_ext += U C^-1 U^T over k-steps [ks0, ks1) of one tile buffer: a warp's blocks, 4
-    // pixels per step, A = U / C (each lane scales by its pixel's 1/C_p), B = U
+    // M_ext += U C^-1 U^T over k-steps [ks0, ks1) of one tile buffer, quad by quad: per
+    // k-step (4 pixels) the A fragments are the row-pair's U words scaled by the lane's
+    // 1/C_p, the B fragments the column-pair's unscaled words (for a diagonal quad the
+    // same words as A); the inner loop is branch-free with immediate shared offsets
     auto gemm = [&](const double* Ub, const double* ic_b, int ks0, int ks1) {
-      if (nmine == MB) {
-        // the common case: every block slot used, so the k-loop has no predication
-        // (no per-MMA warp re-convergence), and A fragments shared by consecutive blocks
-        // of one row are loaded and scaled once
-        for (int ks = ks0; ks < ks1; ++ks) {
-          const int p0 = 4 * ks;
-          const double ic = ic_b[p0 + (lane & 3)];
-          double av[MB], bv[MB];
+      const double* icl = ic_b + (lane & 3);
 #pragma unroll
-          for (int q = 0; q < MB; ++q) {
-            if ((reuseA >> q) & 1u)
-              av[q] = av[q > 0 ? q - 1 : 0];
-            else
-              av[q] = Ub[offA[q] + p0] * ic;
-            bv[q] = Ub[offB[q] + p0];
+      for (int q = 0; q < QMAX; ++q) {
+        if (q >= nq) break;
+        const double* pr = Ub + fo_r[q];
+        if (qr[q] == qc[q]) {
+#pragma unroll 4
+          for (int ks = ks0; ks < ks1; ++ks) {
+            const int p0 = 4 * ks;
+            const double ic = icl[p0];
+            const double b0 = pr[p0], b1 = pr[kRB + p0];
+            const double a0 = b0 * ic, a1 = b1 * ic;
+            dmma884(macc[q][0], a0, b0);
+            dmma884(macc[q][1], a0, b1);
+            dmma884(macc[q][3], a1, b1);
           }
-#pragma unroll
-          for (int q = 0; q < MB; ++q) dmma884(macc[q], av[q], bv[q]);
-        }
-      } else if (nmine > 0) {
-        for (int ks = ks0; ks < ks1; ++ks) {
-          const int p0 = 4 * ks;
-          const double ic = ic_b[p0 + (lane & 3)];
-#pragma unroll
-          for (int q = 0; q < MB; ++q) {
-            if (q < nmine) {
-              const double av = Ub[offA[q] + p0] * ic;
-              const double bv = Ub[offB[q] + p0];
-              dmma884(macc[q], av, bv);
-            }
+        } else {
+          const double* pc = Ub + fo_c[q];
+#pragma unroll 4
+          for (int ks = ks0; ks < ks1; ++ks) {
+            const int p0 = 4 * ks;
+            const double ic = icl[p0];
+            const double a0 = pr[p0] * ic, a1 = pr[kRB + p0] * ic;
+            const double b0 = pc[p0], b1 = pc[kRB + p0];
+            dmma884(macc[q][0], a0, b0);
+            dmma884(macc[q][1], a0, b1);
+            dmma884(macc[q][2], a1, b0);
+            dmma884(macc[q][3], a1, b1);
           }
         }
       }
@@ -671,25 +700,29 @@ __global__ void __launch_bounds__(kPassThreads, 1) pass_kernel(const PassArgs A)
     double* pM = A.part_M + A.seg_off_M[sg];
     double* pw = A.part_w + A.seg_off_w[sg];
 #pragma unroll
-    for (int q = 0; q < MB; ++q) {
-      if (q >= nmine) continue;
-      const int bi = (offA[q] / US) >> 3, bj = (offB[q] / US) >> 3;
+    for (int q = 0; q < QMAX; ++q) {
+      if (q >= nq) continue;
 #pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        const int R = 8 * bi + (lane >> 2), Cc = 8 * bj + 2 * (lane & 3) + i;
-        if (R > Cc || Cc >= mext) continue;
-        const double v = macc[q][i];
-        if (Cc < mu) {
-          pM[(long long)R * mu + Cc] = v;
-          pM[(long long)Cc * mu + R] = v;
-        } else if (R < mu && Cc == mu) {
-          pw[R] = v;
-        } else if (R < mu && Cc == mu + 1) {
-          pw[mu + R] = v;
-        } else if (R == mu && Cc == mu + 1) {
-          pf[16] = v;  // rho
-        } else if (R == mu + 1 && Cc == mu + 1) {
-          pf[15] = v;  // gamma
+      for (int b = 0; b < 4; ++b) {
+        if (b == 2 && qr[q] == qc[q]) continue;  // (2r+1, 2r): the transpose of block 1
+        const int bi = 2 * qr[q] + (b >> 1), bj = 2 * qc[q] + (b & 1);
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const int R = 8 * bi + (lane >> 2), Cc = 8 * bj + 2 * (lane & 3) + i;
+          if (R > Cc || Cc >= mext) continue;
+          const double v = macc[q][b][i];
+          if (Cc < mu) {
+            pM[(long long)R * mu + Cc] = v;
+            pM[(long long)Cc * mu + R] = v;
+          } else if (R < mu && Cc == mu) {
+            pw[R] = v;
+          } else if (R < mu && Cc == mu + 1) {
+            pw[mu + R] = v;
+          } else if (R == mu && Cc == mu + 1) {
+            pf[16] = v;  // rho
+          } else if (R == mu + 1 && Cc == mu + 1) {
+            pf[15] = v;  // gamma
+          }
         }
       }
     }

@@ -33,7 +33,7 @@ from .errors import (CalibrationDegenerateError, CapacityError, ConfigError, Num
 
 DEFAULTS = dict(lambda0=1e-4, lambda_min=1e-8, lambda_max=1e6, eta=1e-4, alpha=1e-3,
                 d_min=1e-6, tangent_max=1.0, calib_cond_max=1e8, damping_candidates=0,
-                refine=True)
+                refine=False)
 
 
 # ----------------------------------------------------------------------------- SPEC types
