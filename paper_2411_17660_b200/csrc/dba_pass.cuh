@@ -217,7 +217,7 @@ __device__ __forceinline__ PixTerms pix_terms(const double R[9], const double t[
   const double Y = fma(R[3], qx, fma(R[4], qy, R[5])) + t[1] * d;
   const double Z = fma(R[6], qx, fma(R[7], qy, R[8])) + t[2] * d;
   bool ok = in && Z > 1e-4 * d;  // Z_MIN on the non-homogeneous depth (geometry.py:17)
-  o.iz = ok ? __drcp_rn(Z) : 0.0;
+  o.iz = ok ? rcp64(Z) : 0.0;
   o.xt = X * o.iz;
   o.yt = Y * o.iz;
   const double pu = fma(fx, o.xt, cx), pv = fma(fy, o.yt, cy);
