@@ -98,7 +98,7 @@ struct dba_plan {
   int calib = 0, prior = 0, freeze_d = 0, gauge_on = 0, gauge_frame = -1, rank = 0, nranks = 1;
   int scalefix = 0, anchor = -1;  // prior-fixed monocular scale: exact-row step correction
   int f0 = 0, f1 = 0, NL = 0, EL = 0, kmax = 0, nb = 0, BW = 0, n_red = 0;
-  int n_tiles = 0, G = 0, nseg = 0, n_units = 0, nve = kEdgeVals, sub = 128, mb = 2, ring = 32;
+  int n_tiles = 0, G = 0, nseg = 0, n_units = 0, nve = kEdgeVals, sub = 128, mb = 3, split = 0, ring = 32;
   size_t pass_smem = 0, solve_smem = 0;
   long long sys_len = 0;  // doubles in one packed reduced system
   long long spec_delta = 0, spec_Lband = 0, spec_rLband = 0, spec_mid = 0;  // per damping candidate
@@ -474,11 +474,14 @@ int dba_plan_create(const dba_problem_desc* d, dba_plan** out) {
       p->sub = 64;
     }
     p->pass_smem = s.total;
-    // quads per warp of the tensor-core product (pass_quads): 2 up to 80 GEMM rows
-    // (radius-5 graphs, with or without intrinsics), 4 up to 112 (out-degree 16)
-    const int qm = pass_qmax(pass_mpad(std::max(p->kmax, 1), p->calib) >> 4);
-    p->mb = qm <= 2 ? 2 : 4;
-    if (p->pass_smem > 225 * 1024 || qm > 4) {
+    // product items per product warp (pass_quads): 3 up to 64 GEMM rows (radius-5
+    // graphs), 4 up to 80 (with intrinsics), 7 up to 112 (out-degree 16)
+    // (the finer split only where it needs no more items per warp)
+    const int np = pass_mpad(std::max(p->kmax, 1), p->calib) >> 4;
+    p->split = pass_qmax(np, true) <= pass_qmax(np, false) ? 1 : 0;
+    const int qm = pass_qmax(np, p->split != 0);
+    p->mb = qm <= 3 ? 3 : qm <= 4 ? 4 : 7;
+    if (p->pass_smem > 225 * 1024 || qm > 7) {
       delete p;
       return DBA_ECAPACITY;
     }
@@ -1043,7 +1046,7 @@ int launch_pass_t(Ctx& c, const PassArgs& a) {
     if (int s = ev_pair(c, ev)) return s;
     DBA_CUDA(cudaEventRecord(pr.pool[ev.first], c.st));
   }
-  if (int s = launch(c, k, dim3(c.p->G), dim3(kPassThreads), c.p->pass_smem, false, a)) return s;
+  if (int s = launch(c, k, dim3(c.p->G), dim3(kPassCTA), c.p->pass_smem, false, a)) return s;
   mark(c, "pass");
   pr.pass_launches++;
   if (!a.runs) pr.pass_runs++;  // gated launches count on the device
@@ -1066,6 +1069,7 @@ int launch_pass(Ctx& c, int cur, int nxt, bool backsub, bool system, bool gated 
   a.n_tiles = p->n_tiles;
   a.kmax = std::max(p->kmax, 1);
   a.sub = p->sub;
+  a.split = p->split;
   a.backsub = backsub ? 1 : 0;
   (void)system;
   a.scalefix = p->scalefix;
@@ -1101,8 +1105,11 @@ int launch_pass(Ctx& c, int cur, int nxt, bool backsub, bool system, bool gated 
   a.seg_off_edge = c.at<long long>(p->L.seg_off_edge);
   a.seg_off_M = c.at<long long>(p->L.seg_off_M);
   a.seg_off_w = c.at<long long>(p->L.seg_off_w);
-  if (p->calib) return p->mb == 2 ? launch_pass_t<true, 2>(c, a) : launch_pass_t<true, 4>(c, a);
-  return p->mb == 2 ? launch_pass_t<false, 2>(c, a) : launch_pass_t<false, 4>(c, a);
+  if (p->calib)
+    return p->mb == 3 ? launch_pass_t<true, 3>(c, a) : p->mb == 4 ? launch_pass_t<true, 4>(c, a)
+                                                             : launch_pass_t<true, 7>(c, a);
+  return p->mb == 3 ? launch_pass_t<false, 3>(c, a) : p->mb == 4 ? launch_pass_t<false, 4>(c, a)
+                                                            : launch_pass_t<false, 7>(c, a);
 }
 
 // LM controller inputs: the trial (slot 1) energy, the flags word and the options

@@ -45,13 +45,25 @@
 
 namespace dba {
 
-constexpr int kPassThreads = 256;
+constexpr int kPassThreads = 256;  // linearisation (geometry) threads
 constexpr int kPassWarps = 8;
+constexpr int kGemmWarps = 4;      // one warpgroup: the tensor-core Schur product
+constexpr int kGemmThreads = 32 * kGemmWarps;
+constexpr int kPassCTA = kGemmThreads + kPassThreads;
+// named barriers: geometry warps only; U-ring slot b full (geometry -> product warps),
+// slot b empty (product -> geometry)
+constexpr int kBarGeo = 1, kBarFull = 2, kBarEmpty = 4;
+// register split between the roles (setmaxnreg; 128 * R_gemm + 256 * R_geo <= 384 * 168)
+__host__ __device__ constexpr int pass_gemm_regs(int qmax) { return qmax <= 3 ? 96 : qmax <= 4 ? 112 : 160; }
+__host__ __device__ constexpr int pass_geo_regs(int qmax) {
+  return ((384 * 168 - 128 * pass_gemm_regs(qmax)) / 256) & ~7;
+}
 constexpr int kSlice = 32;     // pixels per phase-B edge unit (1 per lane)
 constexpr int kEdgeSlots = 2;  // distinct edges per warp per segment (see pass_units)
 
 struct PassArgs {
   int H, W, P, n_tiles, kmax, sub;
+  int split;    // product item split (pass_quads)
   int backsub;  // run phase A
   int freeze;   // disparity block frozen (motion-only / pose stage): no Schur fill-in, d unchanged
   int scalefix; // prior-fixed monocular scale: the A5 column carries c = d (eta + alpha m) instead
@@ -112,25 +124,32 @@ __host__ __device__ inline int pass_mpad(int k, bool calib) { return (pass_mext(
 __host__ __device__ constexpr int pass_ustride(int sub) { return sub + 4; }
 
 // Work split of the symmetric product M_ext = V C^-1 V^T (upper triangle, 8x8 blocks).
-// The np = mpad/16 row PAIRS of blocks form quads: a cross quad (r < c) is the 2x2 block
-// square {2r, 2r+1} x {2c, 2c+1} (4 fragments loaded, 4 DMMAs per k-step), a diagonal
-// quad (r = c) the blocks (2r,2r), (2r,2r+1), (2r+1,2r+1) (2 fragments: A and B
-// fragments of one block row are the same shared-memory words, 3 DMMAs).  Quads go to
-// the 8 warps longest-first (cross, then diagonal) onto the least-loaded warp, lowest
-// index on ties; every thread evaluates the same deterministic assignment.
-// Returns the number of quads of warp `w`, their pairs in (qr, qc) when non-null.
+// The np = mpad/16 row PAIRS of blocks give three kinds of items:
+//   cross (r < c): the 2x2 block square {2r, 2r+1} x {2c, 2c+1}: 4 fragments, 4 DMMAs
+//   dpair (r = c): the diagonal blocks (2r,2r), (2r+1,2r+1): 2 fragments, 2 DMMAs
+//   doff  (r = c): the block (2r, 2r+1): 2 fragments, 1 DMMA
+// (A and B fragments of one block row are the same shared-memory words.)  Items go to
+// the kGemmWarps product warps longest-first onto the least-loaded warp, lowest index on
+// ties (np = 4, radius-5 graphs, unsplit: 8, 8, 10, 10 DMMAs per k-step; split: 9 each
+// but 4 items on some warps, i.e. more accumulator registers).  Without `split` a diagonal pair is
+// one item, (2r,2r), (2r,2r+1), (2r+1,2r+1) (kind 3: 2 fragments, 3 DMMAs): fewer items
+// per warp (registers) at a coarser balance.  Every thread evaluates the same
+// deterministic assignment.  Returns the number of items of warp `w`, their pairs and
+// kinds (0 cross, 1 dpair, 2 doff, 3 diag) in (qr, qc, qk) when non-null.
 template <int QMAX>
-__host__ __device__ inline int pass_quads(int np, int w, int* qr, int* qc) {
-  int load[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+__host__ __device__ inline int pass_quads(int np, int w, bool split, int* qr, int* qc, int* qk) {
+  constexpr int nw = kGemmWarps;
+  int load[nw];
+  for (int x = 0; x < nw; ++x) load[x] = 0;
   int n = 0;
-  for (int pass = 0; pass < 2; ++pass)
+  for (int kind = 0; kind < 4; ++kind)
     for (int r = 0; r < np; ++r)
       for (int c = r; c < np; ++c) {
-        if ((pass == 0) != (r < c)) continue;
+        if ((kind == 0) != (r < c) || (kind == 3 && split) || ((kind == 1 || kind == 2) && !split)) continue;
         int best = 0;
-        for (int x = 1; x < 8; ++x)
+        for (int x = 1; x < nw; ++x)
           if (load[x] < load[best]) best = x;
-        load[best] += r < c ? 4 : 3;
+        load[best] += kind == 0 ? 4 : kind == 1 ? 2 : kind == 2 ? 1 : 3;
         if (best == w) {
           if (qr) {
 #pragma unroll
@@ -138,6 +157,7 @@ __host__ __device__ inline int pass_quads(int np, int w, int* qr, int* qc) {
               if (s == n) {
                 qr[s] = r;
                 qc[s] = c;
+                qk[s] = kind;
               }
           }
           ++n;
@@ -145,10 +165,13 @@ __host__ __device__ inline int pass_quads(int np, int w, int* qr, int* qc) {
       }
   return n;
 }
-// largest per-warp quad count for np row pairs (the plan picks QMAX from it)
-__host__ __device__ inline int pass_qmax(int np) {
+// largest per-warp item count for np row pairs (the plan picks QMAX from it)
+__host__ __device__ inline int pass_qmax(int np, bool split) {
   int m = 0;
-  for (int w = 0; w < 8; ++w) m = pass_quads<1>(np, w, nullptr, nullptr) > m ? pass_quads<1>(np, w, nullptr, nullptr) : m;
+  for (int w = 0; w < kGemmWarps; ++w) {
+    const int n = pass_quads<1>(np, w, split, nullptr, nullptr, nullptr);
+    m = n > m ? n : m;
+  }
   return m;
 }
 
@@ -245,8 +268,73 @@ __device__ __forceinline__ void theta_jac(const double R[9], const PixTerms& T, 
   Tv[3] = 1.0 - cv1;
 }
 
+
+// The product warp's k-loop for a compile-time item shape: NC cross items then ND
+// diagonal items, k-step outer and items inner, so every accumulator chain of the warp is
+// in flight at once (a lone product warp per SM sub-partition has no other warp to hide
+// the DMMA latency behind) with no branches inside the loop.
+template <int QMAX, int US, int NC, int ND>
+__device__ __forceinline__ void gemm_shape(double (&macc)[QMAX][4][2], const double* Ub, const double* icl,
+                                           const int (&fo_r)[QMAX], const int (&fo_c)[QMAX]) {
+  constexpr int kRB = 8 * US;
+  constexpr int nks = (US - 4) / 4;
+#pragma unroll 2
+  for (int ks = 0; ks < nks; ++ks) {
+    const int p0 = 4 * ks;
+    const double ic = icl[p0];
+#pragma unroll
+    for (int i = 0; i < NC; ++i) {
+      const double* pr = Ub + fo_r[i] + p0;
+      const double* pc = Ub + fo_c[i] + p0;
+      const double a0 = pr[0] * ic, a1 = pr[kRB] * ic;
+      const double c0 = pc[0], c1 = pc[kRB];
+      dmma884(macc[i][0], a0, c0);
+      dmma884(macc[i][1], a0, c1);
+      dmma884(macc[i][2], a1, c0);
+      dmma884(macc[i][3], a1, c1);
+    }
+#pragma unroll
+    for (int j = 0; j < ND; ++j) {
+      const double* pr = Ub + fo_r[NC + j] + p0;
+      const double r0 = pr[0], r1 = pr[kRB];
+      const double a0 = r0 * ic;
+      dmma884(macc[NC + j][0], a0, r0);
+      dmma884(macc[NC + j][1], a0, r1);
+      dmma884(macc[NC + j][3], r1 * ic, r1);
+    }
+  }
+}
+// runs gemm_shape<NC', ND'> for the runtime (nc, nd); false when the shape is not covered
+template <int QMAX, int US, int NC, int ND>
+__device__ __forceinline__ bool gemm_dispatch(int nc, int nd, double (&macc)[QMAX][4][2], const double* Ub,
+                                              const double* icl, const int (&fo_r)[QMAX], const int (&fo_c)[QMAX]) {
+  if (nc == NC && nd == ND) {
+    gemm_shape<QMAX, US, NC, ND>(macc, Ub, icl, fo_r, fo_c);
+    return true;
+  }
+  if constexpr (NC + ND + 1 <= QMAX && QMAX <= 4) {
+    if (gemm_dispatch<QMAX, US, NC, ND + 1>(nc, nd, macc, Ub, icl, fo_r, fo_c)) return true;
+    if constexpr (ND == 0)
+      if (gemm_dispatch<QMAX, US, NC + 1, 0>(nc, nd, macc, Ub, icl, fo_r, fo_c)) return true;
+  }
+  return false;
+}
+
+__device__ __forceinline__ void nbar_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void nbar_arrive(int id, int n) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+// Warp-specialised: warpgroup 0 (kGemmWarps warps) runs the tensor-core product, the
+// other 8 warps the per-pixel linearisation.  Per tile the geometry warps fill U-ring
+// slot b (tile sequence number & 1) and hand it over (kBarFull + b); the product warps
+// drain it and hand it back (kBarEmpty + b).  DMMA and DFMA share the fp64 datapath
+// (profiles/tools/mb_fp64pipes.cu), so the point is that every SM sub-partition always has
+// a warp with fp64 work ready: one product warp next to two linearisation warps.
 template <bool CALIB, int QMAX, int SUB>
-__global__ void __launch_bounds__(kPassThreads, 1) pass_kernel(const PassArgs A) {
+__global__ void __launch_bounds__(kPassCTA, 1) pass_kernel(const PassArgs A) {
   pdl_enter();
   if (trial_skipped(A.status)) return;
   if (A.runs && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(A.runs, 1ull);
@@ -255,14 +343,153 @@ __global__ void __launch_bounds__(kPassThreads, 1) pass_kernel(const PassArgs A)
   constexpr int SL = SUB / kSlice, US = pass_ustride(SUB);
   const PassSmem L = pass_smem_layout(A.kmax, CALIB, SUB);
   float4* fbuf = reinterpret_cast<float4*>(smem + L.fbuf);  // [k][SUB] flow records
-  // two column-major [mpad][US] buffers: phase B of tile t fills one while the tensor-core
-  // product of tile t-1 drains the other (DMMA and DFMA are separate pipes on B200)
-  double* const Ubuf = reinterpret_cast<double*>(smem + L.U);
+  double* const Ubuf = reinterpret_cast<double*>(smem + L.U);  // U ring: two [mpad][US] slots
   const int ulen = pass_mpad(A.kmax, CALIB) * US;
+  double* const icvb = reinterpret_cast<double*>(smem + L.icv);  // 1 / C_p, per ring slot
+  const int sg0 = A.cta_seg[blockIdx.x], sg1 = A.cta_seg[blockIdx.x + 1];
+  int ntot = 0;  // tiles of this CTA: the ring handshakes
+  for (int sg = sg0; sg < sg1; ++sg) ntot += A.seg_t1[sg] - A.seg_t0[sg];
+  constexpr int nks = SUB / 4;
+
+  if (threadIdx.x < kGemmThreads) {
+    // ============================================================== product warps
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(pass_gemm_regs(QMAX)));
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int tau = 0;
+    for (int sg = sg0; sg < sg1; ++sg) {
+      const int fl = A.seg_frame[sg];
+      const int k = A.csr_off[fl + 1] - A.csr_off[fl];
+      const int mu = pass_mu(k, CALIB);
+      const int mext = mu + 2;
+      const int np = ((mext + 15) & ~15) >> 4;
+      double* pf = A.part_frame + (long long)sg * kFrameVals;
+      // product items of this warp (pass_quads): fragment pointers into a ring slot are
+      // U + fo_r[q] (rows of block 2r; block 2r+1 is kRB doubles further) and U + fo_c[q]
+      int qr[QMAX], qc[QMAX], qk[QMAX];
+#pragma unroll
+      for (int q = 0; q < QMAX; ++q) qr[q] = qc[q] = qk[q] = 0;
+      const int nq = pass_quads<QMAX>(np, warp, A.split != 0, qr, qc, qk);
+      const int lane_off = (lane >> 2) * US + (lane & 3);
+      int fo_r[QMAX], fo_c[QMAX];
+#pragma unroll
+      for (int q = 0; q < QMAX; ++q) {
+        fo_r[q] = 16 * qr[q] * US + lane_off;
+        fo_c[q] = 16 * qc[q] * US + lane_off;
+      }
+      constexpr int kRB = 8 * US;  // doubles between the fragments of blocks 2r and 2r+1
+      double macc[QMAX][4][2];
+#pragma unroll
+      for (int q = 0; q < QMAX; ++q)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) macc[q][b][0] = macc[q][b][1] = 0.0;
+      // M_ext += U C^-1 U^T over the k-steps of one ring slot, item by item: per k-step
+      // (4 pixels) the A fragments are the row-pair's U words scaled by the lane's 1/C_p,
+      // the B fragments the column-pair's unscaled words (for a diagonal item the same
+      // words as A); branch-free inner loops with immediate shared offsets
+      int nc = 0;  // items are in kind order: cross (kind 0) first, then diagonal (3)
+#pragma unroll
+      for (int q = 0; q < QMAX; ++q) nc += (q < nq && qk[q] == 0) ? 1 : 0;
+      auto gemm = [&](const double* Ub, const double* ic_b) {
+        const double* icl = ic_b + (lane & 3);
+        if (QMAX <= 4 && !A.split && gemm_dispatch<QMAX, US, 0, 0>(nc, nq - nc, macc, Ub, icl, fo_r, fo_c))
+          return;
+        // generic: item by item, branch-free unrolled k-loops per item
+#pragma unroll
+        for (int q = 0; q < QMAX; ++q) {
+          if (q >= nq) break;
+          const double* pr = Ub + fo_r[q];
+          if (qk[q] == 1) {  // (2r,2r), (2r+1,2r+1)
+#pragma unroll 4
+            for (int ks = 0; ks < nks; ++ks) {
+              const int p0 = 4 * ks;
+              const double ic = icl[p0];
+              const double b0 = pr[p0], b1 = pr[kRB + p0];
+              dmma884(macc[q][0], b0 * ic, b0);
+              dmma884(macc[q][3], b1 * ic, b1);
+            }
+          } else if (qk[q] == 3) {  // (2r,2r), (2r,2r+1), (2r+1,2r+1)
+#pragma unroll 4
+            for (int ks = 0; ks < nks; ++ks) {
+              const int p0 = 4 * ks;
+              const double ic = icl[p0];
+              const double b0 = pr[p0], b1 = pr[kRB + p0];
+              const double a0 = b0 * ic;
+              dmma884(macc[q][0], a0, b0);
+              dmma884(macc[q][1], a0, b1);
+              dmma884(macc[q][3], b1 * ic, b1);
+            }
+          } else if (qk[q] == 2) {  // (2r, 2r+1)
+#pragma unroll 4
+            for (int ks = 0; ks < nks; ++ks) {
+              const int p0 = 4 * ks;
+              const double ic = icl[p0];
+              dmma884(macc[q][1], pr[p0] * ic, pr[kRB + p0]);
+            }
+          } else {
+            const double* pc = Ub + fo_c[q];
+#pragma unroll 4
+            for (int ks = 0; ks < nks; ++ks) {
+              const int p0 = 4 * ks;
+              const double ic = icl[p0];
+              const double a0 = pr[p0] * ic, a1 = pr[kRB + p0] * ic;
+              const double b0 = pc[p0], b1 = pc[kRB + p0];
+              dmma884(macc[q][0], a0, b0);
+              dmma884(macc[q][1], a0, b1);
+              dmma884(macc[q][2], a1, b0);
+              dmma884(macc[q][3], a1, b1);
+            }
+          }
+        }
+      };
+      for (int tile = A.seg_t0[sg]; tile < A.seg_t1[sg]; ++tile, ++tau) {
+        const int b = tau & 1;
+        nbar_sync(kBarFull + b, kPassCTA);
+        gemm(Ubuf + b * ulen, icvb + b * SUB);
+        if (tau + 2 < ntot) nbar_arrive(kBarEmpty + b, kPassCTA);
+      }
+    // tensor-core blocks -> M (mu x mu, both triangles), w = column mu, h = column mu+1,
+    // rho, gamma; lane l holds D[l/4][2(l%4) + i] of each block
+    double* pM = A.part_M + A.seg_off_M[sg];
+    double* pw = A.part_w + A.seg_off_w[sg];
+#pragma unroll
+    for (int q = 0; q < QMAX; ++q) {
+      if (q >= nq) continue;
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        // blocks of the item: cross all four, dpair 0 and 3, doff 1, diag 0, 1 and 3
+        if (qk[q] == 1 && (b == 1 || b == 2)) continue;
+        if (qk[q] == 3 && b == 2) continue;
+        if (qk[q] == 2 && b != 1) continue;
+        const int bi = 2 * qr[q] + (b >> 1), bj = 2 * qc[q] + (b & 1);
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const int R = 8 * bi + (lane >> 2), Cc = 8 * bj + 2 * (lane & 3) + i;
+          if (R > Cc || Cc >= mext) continue;
+          const double v = macc[q][b][i];
+          if (Cc < mu) {
+            pM[(long long)R * mu + Cc] = v;
+            pM[(long long)Cc * mu + R] = v;
+          } else if (R < mu && Cc == mu) {
+            pw[R] = v;
+          } else if (R < mu && Cc == mu + 1) {
+            pw[mu + R] = v;
+          } else if (R == mu && Cc == mu + 1) {
+            pf[16] = v;  // rho
+          } else if (R == mu + 1 && Cc == mu + 1) {
+            pf[15] = v;  // gamma
+          }
+        }
+      }
+    }
+    }  // segments
+    return;
+  }
+
+  // ================================================================ linearisation warps
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(pass_geo_regs(QMAX)));
   double* parts = reinterpret_cast<double*>(smem + L.parts);
   double* dcs = reinterpret_cast<double*>(smem + L.dcs);
   double* dns = reinterpret_cast<double*>(smem + L.dns);
-  double* const icvb = reinterpret_cast<double*>(smem + L.icv);  // 1 / C_p, per tile buffer
   double2* qcs = reinterpret_cast<double2*>(smem + L.qc);  // normalised pixel rays at x_c
   double2* qns = reinterpret_cast<double2*>(smem + L.qn);  // ... at x_n
   double* ebuf = reinterpret_cast<double*>(smem + L.ebuf);
@@ -273,14 +500,15 @@ __global__ void __launch_bounds__(kPassThreads, 1) pass_kernel(const PassArgs A)
   EdgeLin* sl = reinterpret_cast<EdgeLin*>(smem + L.sl);
   EdgeBack* sb = reinterpret_cast<EdgeBack*>(smem + L.sb);
 
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = threadIdx.x - kGemmThreads, lane = tid & 31, warp = tid >> 5;
   const int P = A.P, KM = A.kmax;
   const double Wf = (double)A.W, Hf = (double)A.H;
   const double fxn = A.intr_n[0], fyn = A.intr_n[1], cxn = A.intr_n[2], cyn = A.intr_n[3];
   const double fxc = A.intr_c[0], fyc = A.intr_c[1], cxc = A.intr_c[2], cyc = A.intr_c[3];
   const double dth[4] = {fxn - fxc, fyn - fyc, cxn - cxc, cyn - cyc};
+  int tau = 0;
 
-  for (int sg = A.cta_seg[blockIdx.x]; sg < A.cta_seg[blockIdx.x + 1]; ++sg) {
+  for (int sg = sg0; sg < sg1; ++sg) {
     const int fl = A.seg_frame[sg];
     const int s0 = A.csr_off[fl];
     const int k = A.csr_off[fl + 1] - s0;
@@ -310,31 +538,6 @@ __global__ void __launch_bounds__(kPassThreads, 1) pass_kernel(const PassArgs A)
       ebuf[x] = 0.0;
       if (CALIB) ethb[x] = 0.0;
     }
-    // padding columns of U (mext..mpad) stay zero for the whole segment
-    for (int x = tid; x < 2 * (mpad - mext) * SUB; x += kPassThreads) {
-      const int y = x % ((mpad - mext) * SUB);
-      Ubuf[(x >= (mpad - mext) * SUB ? ulen : 0) + (mext + y / SUB) * US + y % SUB] = 0.0;
-    }
-    // tensor-core quads of this warp (pass_quads): fragment pointers into a U buffer are
-    // U + fo_r[q] (rows of block 2r; block 2r+1 is kRB doubles further) and U + fo_c[q]
-    const int np = mpad >> 4;
-    int qr[QMAX], qc[QMAX];
-#pragma unroll
-    for (int q = 0; q < QMAX; ++q) qr[q] = qc[q] = 0;
-    const int nq = pass_quads<QMAX>(np, warp, qr, qc);
-    const int lane_off = (lane >> 2) * US + (lane & 3);
-    int fo_r[QMAX], fo_c[QMAX];
-#pragma unroll
-    for (int q = 0; q < QMAX; ++q) {
-      fo_r[q] = 16 * qr[q] * US + lane_off;
-      fo_c[q] = 16 * qc[q] * US + lane_off;
-    }
-    constexpr int kRB = 8 * US;  // doubles between the fragments of blocks 2r and 2r+1
-    double macc[QMAX][4][2];
-#pragma unroll
-    for (int q = 0; q < QMAX; ++q)
-#pragma unroll
-      for (int b = 0; b < 4; ++b) macc[q][b][0] = macc[q][b][1] = 0.0;
     double hacc[kEdgeSlots][28];  // per-edge H_jj, g_j, energy of this warp's units (whole segment)
 #pragma unroll
     for (int s = 0; s < kEdgeSlots; ++s)
@@ -346,7 +549,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) pass_kernel(const PassArgs A)
     double fpri = 0.0;  // scalefix: sum_p d_p alpha m_p (d*_p - d_p) (the prior's gradient along the scale)
     // A5: kappa = (rho - h . delta_local) / gamma from the x_c linearisation
     const bool gauge = (f == A.gauge_frame) && k > 0;
-    __syncthreads();
+    nbar_sync(kBarGeo, kPassThreads);
     double kappa = 0.0;
     if (gauge && A.backsub) {
       const double* gs = A.gstate_c;
@@ -357,45 +560,6 @@ __global__ void __launch_bounds__(kPassThreads, 1) pass_kernel(const PassArgs A)
         for (int q = 0; q < 4; ++q) hd += gs[2 + 6 * k + q] * dth[q];
       kappa = (gs[1] - hd) / gs[0];
     }
-
-    // M_ext += U C^-1 U^T over k-steps [ks0, ks1) of one tile buffer, quad by quad: per
-    // k-step (4 pixels) the A fragments are the row-pair's U words scaled by the lane's
-    // 1/C_p, the B fragments the column-pair's unscaled words (for a diagonal quad the
-    // same words as A); the inner loop is branch-free with immediate shared offsets
-    auto gemm = [&](const double* Ub, const double* ic_b, int ks0, int ks1) {
-      const double* icl = ic_b + (lane & 3);
-#pragma unroll
-      for (int q = 0; q < QMAX; ++q) {
-        if (q >= nq) break;
-        const double* pr = Ub + fo_r[q];
-        if (qr[q] == qc[q]) {
-#pragma unroll 4
-          for (int ks = ks0; ks < ks1; ++ks) {
-            const int p0 = 4 * ks;
-            const double ic = icl[p0];
-            const double b0 = pr[p0], b1 = pr[kRB + p0];
-            const double a0 = b0 * ic, a1 = b1 * ic;
-            dmma884(macc[q][0], a0, b0);
-            dmma884(macc[q][1], a0, b1);
-            dmma884(macc[q][3], a1, b1);
-          }
-        } else {
-          const double* pc = Ub + fo_c[q];
-#pragma unroll 4
-          for (int ks = ks0; ks < ks1; ++ks) {
-            const int p0 = 4 * ks;
-            const double ic = icl[p0];
-            const double a0 = pr[p0] * ic, a1 = pr[kRB + p0] * ic;
-            const double b0 = pc[p0], b1 = pc[kRB + p0];
-            dmma884(macc[q][0], a0, b0);
-            dmma884(macc[q][1], a0, b1);
-            dmma884(macc[q][2], a1, b0);
-            dmma884(macc[q][3], a1, b1);
-          }
-        }
-      }
-    };
-    const int nks = SUB / 4;
 
     // cp.async staging of a tile's flow records (16 B each) and disparities;
     // out-of-range pixels are zero-filled
@@ -418,14 +582,11 @@ __global__ void __launch_bounds__(kPassThreads, 1) pass_kernel(const PassArgs A)
     };
     prefetch(A.seg_t0[sg]);
 
-    for (int tile = A.seg_t0[sg]; tile < A.seg_t1[sg]; ++tile) {
+    for (int tile = A.seg_t0[sg]; tile < A.seg_t1[sg]; ++tile, ++tau) {
       const int pbase = tile * SUB;
-      const int tb = (tile - A.seg_t0[sg]) & 1;
-      double* const U = Ubuf + tb * ulen;  // this tile's buffer
+      const int tb = tau & 1;
+      double* const U = Ubuf + tb * ulen;  // this tile's ring slot
       double* const icv = icvb + tb * SUB;
-      const bool drain = tile > A.seg_t0[sg];  // the previous tile's product is pending
-      const double* const Up = Ubuf + (tb ^ 1) * ulen;
-      const double* const icp = icvb + (tb ^ 1) * SUB;
       asm volatile("cp.async.wait_all;" ::: "memory");
       for (int x = tid; x < SUB; x += kPassThreads) {
         const int p = pbase + x;
@@ -433,7 +594,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) pass_kernel(const PassArgs A)
         qcs[x] = make_double2((pu - cxc) / fxc, (pv - cyc) / fyc);
         qns[x] = make_double2((pu - cxn) / fxn, (pv - cyn) / fyn);
       }
-      __syncthreads();
+      nbar_sync(kBarGeo, kPassThreads);
       // ------------------------------------------------------------ phase A
       // pixel-major: a half-warp per 16 pixels, the two halves split the edges; the
       // per-pixel sums close with one shuffle, so d_n needs no block barrier
@@ -500,18 +661,10 @@ __global__ void __launch_bounds__(kPassThreads, 1) pass_kernel(const PassArgs A)
           if (p < P) A.d_new[(size_t)f * P + p] = dcs[x];
         }
       }
-      __syncthreads();
+      nbar_sync(kBarGeo, kPassThreads);
       // ------------------------------------------------------------ phase B
-      // the previous tile's tensor-core k-steps are spread over this warp's units: the
-      // DMMAs issue between the float64 geometry and drain in the background
-      const int kper = u1 > u0 ? (nks + (u1 - u0) - 1) / (u1 - u0) : 0;
-      int ksd = 0;
+      if (tau >= 2) nbar_sync(kBarEmpty + tb, kPassCTA);  // the product warps are done with the slot
       for (int u = u0; u < u1; ++u) {
-        if (drain) {
-          const int ks1 = min(ksd + kper, nks);
-          gemm(Up, icp, ksd, ks1);
-          ksd = ks1;
-        }
         const int a = u / SL, slot = a - e0;
         const int pl = (u - a * SL) * kSlice + lane, p = pbase + pl;
         const bool in = p < P;
@@ -602,8 +755,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) pass_kernel(const PassArgs A)
           ethb[(warp * kEdgeSlots + slot) * 32 + lane] += rs;
         }
       }
-      if (drain) gemm(Up, icp, ksd, nks);  // warps without units (or a remainder)
-      __syncthreads();
+      nbar_sync(kBarGeo, kPassThreads);
       if (tile + 1 < A.seg_t1[sg]) prefetch(tile + 1);  // overlaps the rest of the tile
       // ------------------------------------------------------------ per pixel
       // C_p, g_d,p (+ Eq. 4 prior), 1/C_p and the extra columns; the 1/C_p scaling is
@@ -642,13 +794,9 @@ __global__ void __launch_bounds__(kPassThreads, 1) pass_kernel(const PassArgs A)
         U[mu * US + pl] = gd;
         U[(mu + 1) * US + pl] = in ? cx : 0.0;
       }
-      __syncthreads();
-      // (phase C of this tile runs interleaved with the next tile's phase B)
-    }
-    __syncthreads();  // the last tile's 1/C_p and extra columns
-    {  // ------------------------------------------------------------ phase C, last tile
-      const int tb = (A.seg_t1[sg] - 1 - A.seg_t0[sg]) & 1;
-      gemm(Ubuf + tb * ulen, icvb + tb * SUB, 0, nks);
+      // rows mext..mpad of the slot: zero (the product covers whole 16-row pairs)
+      for (int x = tid; x < (mpad - mext) * SUB; x += kPassThreads) U[(mext + x / SUB) * US + x % SUB] = 0.0;
+      nbar_arrive(kBarFull + tb, kPassCTA);
     }
 
     // ------------------------------------------------------------ segment outputs
@@ -677,7 +825,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) pass_kernel(const PassArgs A)
       for (int off = 16; off >= 1; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
       if (lane == 0) red[warp * 16 + 15] = v;
     }
-    __syncthreads();
+    nbar_sync(kBarGeo, kPassThreads);
     double* pf = A.part_frame + (long long)sg * kFrameVals;
     if (tid < kFrameVals) {
       double v = 0.0;
@@ -695,38 +843,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) pass_kernel(const PassArgs A)
         if (emap[ws] == a) v += (l < 32) ? ebuf[ws * 32 + l] : ethb[ws * 32 + (l - 32)];
       pe[x] = v;
     }
-    // tensor-core blocks -> M (mu x mu, both triangles), w = column mu, h = column mu+1,
-    // rho, gamma; lane l holds D[l/4][2(l%4) + i] of each block
-    double* pM = A.part_M + A.seg_off_M[sg];
-    double* pw = A.part_w + A.seg_off_w[sg];
-#pragma unroll
-    for (int q = 0; q < QMAX; ++q) {
-      if (q >= nq) continue;
-#pragma unroll
-      for (int b = 0; b < 4; ++b) {
-        if (b == 2 && qr[q] == qc[q]) continue;  // (2r+1, 2r): the transpose of block 1
-        const int bi = 2 * qr[q] + (b >> 1), bj = 2 * qc[q] + (b & 1);
-#pragma unroll
-        for (int i = 0; i < 2; ++i) {
-          const int R = 8 * bi + (lane >> 2), Cc = 8 * bj + 2 * (lane & 3) + i;
-          if (R > Cc || Cc >= mext) continue;
-          const double v = macc[q][b][i];
-          if (Cc < mu) {
-            pM[(long long)R * mu + Cc] = v;
-            pM[(long long)Cc * mu + R] = v;
-          } else if (R < mu && Cc == mu) {
-            pw[R] = v;
-          } else if (R < mu && Cc == mu + 1) {
-            pw[mu + R] = v;
-          } else if (R == mu && Cc == mu + 1) {
-            pf[16] = v;  // rho
-          } else if (R == mu + 1 && Cc == mu + 1) {
-            pf[15] = v;  // gamma
-          }
-        }
-      }
-    }
-    __syncthreads();
+    nbar_sync(kBarGeo, kPassThreads);
   }  // segments
 }
 
