@@ -98,7 +98,7 @@ struct dba_plan {
   int calib = 0, prior = 0, freeze_d = 0, gauge_on = 0, gauge_frame = -1, rank = 0, nranks = 1;
   int scalefix = 0, anchor = -1;  // prior-fixed monocular scale: exact-row step correction
   int f0 = 0, f1 = 0, NL = 0, EL = 0, kmax = 0, nb = 0, BW = 0, n_red = 0;
-  int n_tiles = 0, G = 0, nseg = 0, n_units = 0, nve = kEdgeVals, sub = 128, mb = 3, split = 0, ring = 32;
+  int n_tiles = 0, G = 0, nseg = 0, n_units = 0, nve = kEdgeVals, sub = 128, mb = 3, split = 0, nslot = 2, ring = 32;
   size_t pass_smem = 0, solve_smem = 0;
   long long sys_len = 0;  // doubles in one packed reduced system
   long long spec_delta = 0, spec_Lband = 0, spec_rLband = 0, spec_mid = 0;  // per damping candidate
@@ -466,12 +466,21 @@ int dba_plan_create(const dba_problem_desc* d, dba_plan** out) {
 
   // ---- pass decomposition: G CTAs over (frame, 256-px tile) work items
   {
-    // 128-pixel tiles, 64 when the frame's shared-memory working set would not fit
-    PassSmem s = pass_smem_layout(std::max(p->kmax, 1), p->calib, 128);
+    // 128-pixel tiles with a 2-deep U ring, else 64-pixel tiles with the deepest ring
+    // (<= 4) that fits; DBA_PASS_TILE=64 forces the small tiles (measurement)
+    const int kk = std::max(p->kmax, 1);
+    const char* ft = std::getenv("DBA_PASS_TILE");
+    const bool force64 = ft != nullptr && std::atoi(ft) == 64;
+    PassSmem s = pass_smem_layout(kk, p->calib, 128, 2);
     p->sub = 128;
-    if (s.total > 225 * 1024) {
-      s = pass_smem_layout(std::max(p->kmax, 1), p->calib, 64);
+    p->nslot = 2;
+    if (force64 || s.total > 225 * 1024) {
       p->sub = 64;
+      for (int ns = kMaxSlots; ns >= 2; --ns) {
+        p->nslot = ns;
+        s = pass_smem_layout(kk, p->calib, 64, ns);
+        if (s.total <= 225 * 1024) break;
+      }
     }
     p->pass_smem = s.total;
     // product items per product warp (pass_quads): 3 up to 64 GEMM rows (radius-5
@@ -1070,6 +1079,7 @@ int launch_pass(Ctx& c, int cur, int nxt, bool backsub, bool system, bool gated 
   a.kmax = std::max(p->kmax, 1);
   a.sub = p->sub;
   a.split = p->split;
+  a.nslot = p->nslot;
   a.backsub = backsub ? 1 : 0;
   (void)system;
   a.scalefix = p->scalefix;

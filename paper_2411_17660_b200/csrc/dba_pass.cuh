@@ -52,7 +52,8 @@ constexpr int kGemmThreads = 32 * kGemmWarps;
 constexpr int kPassCTA = kGemmThreads + kPassThreads;
 // named barriers: geometry warps only; U-ring slot b full (geometry -> product warps),
 // slot b empty (product -> geometry)
-constexpr int kBarGeo = 1, kBarFull = 2, kBarEmpty = 4;
+constexpr int kMaxSlots = 4;  // U-ring depth limit (named barriers 2..9)
+constexpr int kBarGeo = 1, kBarFull = 2, kBarEmpty = 2 + kMaxSlots;
 // register split between the roles (setmaxnreg; 128 * R_gemm + 256 * R_geo <= 384 * 168)
 __host__ __device__ constexpr int pass_gemm_regs(int qmax) { return qmax <= 3 ? 96 : qmax <= 4 ? 112 : 160; }
 __host__ __device__ constexpr int pass_geo_regs(int qmax) {
@@ -64,6 +65,7 @@ constexpr int kEdgeSlots = 2;  // distinct edges per warp per segment (see pass_
 struct PassArgs {
   int H, W, P, n_tiles, kmax, sub;
   int split;    // product item split (pass_quads)
+  int nslot;    // U-ring depth (2..kMaxSlots)
   int backsub;  // run phase A
   int freeze;   // disparity block frozen (motion-only / pose stage): no Schur fill-in, d unchanged
   int scalefix; // prior-fixed monocular scale: the A5 column carries c = d (eta + alpha m) instead
@@ -194,16 +196,16 @@ __device__ __forceinline__ void pass_units(int k, int slices, int w, int& u0, in
 struct PassSmem {
   size_t fbuf, U, parts, dcs, dns, icv, qc, qn, ebuf, ethb, red, emap, sflow, sl, sb, total;
 };
-__host__ __device__ inline PassSmem pass_smem_layout(int kmax, bool calib, int sub) {
+__host__ __device__ inline PassSmem pass_smem_layout(int kmax, bool calib, int sub, int nslot) {
   PassSmem s;
   size_t o = 0;
   const int nparts = calib ? 6 : 2;  // phase B: C, gd (+ E_theta x4)
   s.fbuf = o; o += sizeof(float4) * (size_t)kmax * sub;
-  s.U = o; o += 2 * sizeof(double) * (size_t)pass_mpad(kmax, calib) * pass_ustride(sub);  // tile ring
+  s.U = o; o += nslot * sizeof(double) * (size_t)pass_mpad(kmax, calib) * pass_ustride(sub);  // tile ring
   s.parts = o; o += sizeof(double) * (size_t)nparts * kmax * sub;
   s.dcs = o; o += sizeof(double) * sub;
   s.dns = o; o += sizeof(double) * sub;
-  s.icv = o; o += 2 * sizeof(double) * sub;
+  s.icv = o; o += nslot * sizeof(double) * sub;
   s.qc = o; o += sizeof(double2) * sub;
   s.qn = o; o += sizeof(double2) * sub;
   s.ebuf = o; o += sizeof(double) * kPassWarps * kEdgeSlots * 32;
@@ -329,7 +331,7 @@ __device__ __forceinline__ void nbar_arrive(int id, int n) {
 
 // Warp-specialised: warpgroup 0 (kGemmWarps warps) runs the tensor-core product, the
 // other 8 warps the per-pixel linearisation.  Per tile the geometry warps fill U-ring
-// slot b (tile sequence number & 1) and hand it over (kBarFull + b); the product warps
+// slot b (tile sequence number mod the ring depth) and hand it over (kBarFull + b); the product warps
 // drain it and hand it back (kBarEmpty + b).  DMMA and DFMA share the fp64 datapath
 // (profiles/tools/mb_fp64pipes.cu), so the point is that every SM sub-partition always has
 // a warp with fp64 work ready: one product warp next to two linearisation warps.
@@ -341,7 +343,8 @@ __global__ void __launch_bounds__(kPassCTA, 1) pass_kernel(const PassArgs A) {
   extern __shared__ __align__(16) unsigned char smem[];
   constexpr int NVE = kEdgeVals + (CALIB ? kCalibVals : 0);
   constexpr int SL = SUB / kSlice, US = pass_ustride(SUB);
-  const PassSmem L = pass_smem_layout(A.kmax, CALIB, SUB);
+  const int NS = A.nslot;
+  const PassSmem L = pass_smem_layout(A.kmax, CALIB, SUB, NS);
   float4* fbuf = reinterpret_cast<float4*>(smem + L.fbuf);  // [k][SUB] flow records
   double* const Ubuf = reinterpret_cast<double*>(smem + L.U);  // U ring: two [mpad][US] slots
   const int ulen = pass_mpad(A.kmax, CALIB) * US;
@@ -442,10 +445,10 @@ __global__ void __launch_bounds__(kPassCTA, 1) pass_kernel(const PassArgs A) {
         }
       };
       for (int tile = A.seg_t0[sg]; tile < A.seg_t1[sg]; ++tile, ++tau) {
-        const int b = tau & 1;
+        const int b = tau % NS;
         nbar_sync(kBarFull + b, kPassCTA);
         gemm(Ubuf + b * ulen, icvb + b * SUB);
-        if (tau + 2 < ntot) nbar_arrive(kBarEmpty + b, kPassCTA);
+        if (tau + NS < ntot) nbar_arrive(kBarEmpty + b, kPassCTA);
       }
     // tensor-core blocks -> M (mu x mu, both triangles), w = column mu, h = column mu+1,
     // rho, gamma; lane l holds D[l/4][2(l%4) + i] of each block
@@ -584,7 +587,7 @@ __global__ void __launch_bounds__(kPassCTA, 1) pass_kernel(const PassArgs A) {
 
     for (int tile = A.seg_t0[sg]; tile < A.seg_t1[sg]; ++tile, ++tau) {
       const int pbase = tile * SUB;
-      const int tb = tau & 1;
+      const int tb = tau % NS;
       double* const U = Ubuf + tb * ulen;  // this tile's ring slot
       double* const icv = icvb + tb * SUB;
       asm volatile("cp.async.wait_all;" ::: "memory");
@@ -663,7 +666,7 @@ __global__ void __launch_bounds__(kPassCTA, 1) pass_kernel(const PassArgs A) {
       }
       nbar_sync(kBarGeo, kPassThreads);
       // ------------------------------------------------------------ phase B
-      if (tau >= 2) nbar_sync(kBarEmpty + tb, kPassCTA);  // the product warps are done with the slot
+      if (tau >= NS) nbar_sync(kBarEmpty + tb, kPassCTA);  // the product warps are done with the slot
       for (int u = u0; u < u1; ++u) {
         const int a = u / SL, slot = a - e0;
         const int pl = (u - a * SL) * kSlice + lane, p = pbase + pl;
