@@ -14,9 +14,10 @@ value   = edge-pixels/s = E * H * W * (accepted GN iterations per step) / device
           whole job; rejected LM trials are paid for but not counted
 e2e     = the same metric through the public tensor API from pinned HOST buffers
           (flow/disparity/pose H2D + result D2H inside the timed region)
-roofline= the fused pass kernel (dominant kernel): algorithmic bytes per launch
-          (16 B flow record per edge-pixel + 8 B disparity read+write per
-          frame-pixel) / its live CUDA-event launch duration, vs MEASURED_PEAKS
+roofline= the pass kernel (dominant kernel), bound by the float64 datapath: SURVEY §8d
+          algorithmic FLOPs per launch / its live CUDA-event launch duration vs the
+          measured fp64 peak; roofline.hbm = algorithmic bytes (16 B flow record per
+          edge-pixel + 8 B disparity read+write per frame-pixel) vs MEASURED_PEAKS
 cpu_baseline = the float64 numpy oracle (oracle/dba.py, "port") on this host's cores:
           complete GN iterations over the FULL C3 graph (median of 3 after a warm-up);
           --impl reference times the same, one full-graph GN iteration per step, and
@@ -187,32 +188,27 @@ class ClockSampler:
                 "source": "nvml" if self.nvml is not None else "nvidia-smi"}
 
 
+# fp64 datapath peak of this pool's B200, measured (profiles/tools/mb_fp64pipes.cu,
+# profiles/r02_fp64_pipes.txt): DMMA m8n8k4 alone 18.48 TFMA/s, DFMA alone 17.05 TFMA/s, and
+# the two together take the SUM of their times -- the tensor-pipe DMMA and the DFMA pipe are
+# one float64 datapath (64 FMA/clk/SM)
+FP64_PEAK_TFLOPS = 2 * 18.48
+
+
 def compute_roofline(inp, H, W, pass_ms):
-    """FP64-pipe view of the same pass: SURVEY §8d algorithmic FLOPs (230 per edge-pixel
-    for residual/Jacobians/H_jj/E/C, 2 per entry of the per-frame Schur product M_ext = V V^T
-    with 6k+2 rows) against the float64 peak (SMs x 64 FMA x 2 x SM clock; DMMA tensor and
-    DFMA measured at the same 18.5 TFMA/s on this pool)."""
+    """The pass kernel's bound: SURVEY §8d algorithmic FLOPs (230 per edge-pixel for the
+    residual, Jacobians, H_jj, E and C; 2 per entry of the per-frame Schur product
+    M_ext = V C^-1 V^T with 6k+2 rows) per launch over its live launch time, against the
+    measured float64 datapath peak (FP64_PEAK_TFLOPS)."""
     import numpy as np
-    import torch
     P = H * W
     k = np.bincount(np.asarray(inp["ii"])[np.asarray(inp["local"])], minlength=1)
     k = k[k > 0]
     m = 6 * k + 2
     flops = 230.0 * len(inp["local"]) * P + float(np.sum(m * (m + 1))) * P
-    props = torch.cuda.get_device_properties(0)
-    clk_ghz = 1.965
-    try:
-        import pynvml
-        pynvml.nvmlInit()
-        clk_ghz = pynvml.nvmlDeviceGetMaxClockInfo(pynvml.nvmlDeviceGetHandleByIndex(0),
-                                                   pynvml.NVML_CLOCK_SM) / 1000.0
-    except Exception:
-        pass
-    peak = props.multi_processor_count * 64 * 2 * clk_ghz * 1e-3  # TFLOP/s
     achieved = flops / (pass_ms * 1e-3) * 1e-12
-    return {"bound": "fp64", "flop_per_launch": flops, "achieved": achieved, "peak": peak,
-            "unit": "TFLOP/s", "frac": achieved / peak,
-            "peak_kind": "nominal fp64 (64 FMA/clk/SM; measured DFMA and DMMA m8n8k4 both 18.5 TFMA/s)"}
+    return {"flop_per_launch": flops, "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
+            "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS}
 
 
 def build_inputs(keyframes, rank, nranks, partition=None, noise=0.5):
@@ -528,8 +524,7 @@ def main():
                       "ns_per_pivot": s_ms * 1e6 / chain, "reduced_unknowns": 6 * nfree,
                       "note": "two-sided block LDL^T of the banded reduced system (BW=10 blocks on C3), "
                               "one CTA pair per damping candidate (3 candidates, 6 SMs); includes the "
-                              "middle system, both back-substitutions and one iterative-refinement "
-                              "step (residual + forward/middle/backward substitution)"}
+                              "middle system and both back-substitutions"}
 
     # end to end through the public API from pinned host buffers
     e2e = None
@@ -622,22 +617,28 @@ def main():
                             "when accepted"),
             "ms_per_gn_iter": total_ms / max(n_iters, 1),
             "final_energy": rep.final_energy, "initial_energy": rep.initial_energy,
-            "roofline": {"kernel": "dba::pass_kernel (fused back-substitute + linearise + Schur)",
-                         "bound": "hbm", "achieved": achieved, "peak": hbm, "peak_kind": peak_kind,
-                         "unit": "GB/s", "frac": achieved / hbm, "traffic": traffic,
-                         "bytes_per_launch": bytes_per_pass, "ms_per_launch": pass_ms,
-                         "solve_ms_per_launch": stats["solve_ms"] / max(stats["solve_launches"], 1),
-                         "pass_share_of_step": stats["pass_ms"] / max(prof_ms, 1e-9),
-                         "solve_share_of_step": stats["solve_ms"] / max(prof_ms, 1e-9),
-                         # gated-off launches (a few us each) are in the sum: conservative
-                         "energy_pass_ms_per_launch": stats["energy_ms"] / max(prof_energy_runs, 1),
-                         "energy_pass_share_of_step": stats["energy_ms"] / max(prof_ms, 1e-9),
-                         "pass_runs_per_step": stats["pass_runs"] / max(min(args.steps, 5), 1),
-                         "kernel_timing": "CUDA events around each pass/solve/energy launch in "
-                                          f"{min(args.steps, 5)} separate profiled steps",
-                         "compute": compute_roofline(inp, H, W, pass_ms),
-                         "energy_kernel": energy_roofline,
-                         "solve": solve_roofline},
+            "roofline": dict(
+                {"kernel": "dba::pass_kernel (linearise + per-edge Hessians + DMMA Schur fill-in)",
+                 "bound": "tensor",
+                 "datapath": "float64: DMMA m8n8k4 (tensor pipe) and DFMA share one datapath; the "
+                             "per-pixel chain is float64 because float32 measured outside the 1e-4 "
+                             "parity bar (DESIGN.md 5)",
+                 "peak_kind": "measured fp64 DMMA peak (profiles/r02_fp64_pipes.txt)",
+                 "traffic": traffic, "ms_per_launch": pass_ms},
+                **compute_roofline(inp, H, W, pass_ms),
+                **{"hbm": {"achieved": achieved, "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s",
+                           "frac": achieved / hbm, "bytes_per_launch": bytes_per_pass, "traffic": traffic},
+                   "solve_ms_per_launch": stats["solve_ms"] / max(stats["solve_launches"], 1),
+                   "pass_share_of_step": stats["pass_ms"] / max(prof_ms, 1e-9),
+                   "solve_share_of_step": stats["solve_ms"] / max(prof_ms, 1e-9),
+                   # gated-off launches (a few us each) are in the sum: conservative
+                   "energy_pass_ms_per_launch": stats["energy_ms"] / max(prof_energy_runs, 1),
+                   "energy_pass_share_of_step": stats["energy_ms"] / max(prof_ms, 1e-9),
+                   "pass_runs_per_step": stats["pass_runs"] / max(min(args.steps, 5), 1),
+                   "kernel_timing": "CUDA events around each pass/solve/energy launch in "
+                                    f"{min(args.steps, 5)} separate profiled steps",
+                   "energy_kernel": energy_roofline,
+                   "solve": solve_roofline}),
             "gpu_launches": int(timed_launches),
             "e2e": e2e,
             "cpu_baseline": cpu,
