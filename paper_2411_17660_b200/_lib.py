@@ -45,7 +45,7 @@ class Options(ctypes.Structure):
     _fields_ = [
         ("iters", c_i32), ("lambda0", c_dbl), ("lambda_min", c_dbl), ("lambda_max", c_dbl),
         ("eta", c_dbl), ("alpha", c_dbl), ("d_min", c_dbl), ("tangent_max", c_dbl),
-        ("calib_cond_max", c_dbl), ("damping_candidates", c_i32), ("no_refine", c_i32),
+        ("calib_cond_max", c_dbl), ("damping_candidates", c_i32), ("refine", c_i32),
     ]
 
 

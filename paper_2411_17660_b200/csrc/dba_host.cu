@@ -1332,7 +1332,7 @@ int launch_solve(Ctx& c, int slot, int nspec = 1) {
   a.block_pose = c.at<int>(p->L.block_pose);
   a.anchor = p->anchor;
   a.nspec = nspec;
-  a.refine = c.o->no_refine ? 0 : 1;
+  a.refine = c.o->refine ? 1 : 0;
   a.spec_Lband = p->spec_Lband;
   a.spec_rLband = p->spec_rLband;
   a.spec_mid = p->spec_mid;

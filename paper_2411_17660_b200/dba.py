@@ -214,7 +214,7 @@ class DBASolver:
         o.update({k: v for k, v in kw.items() if v is not None})
         return _lib.Options(int(iters), o["lambda0"], o["lambda_min"], o["lambda_max"], o["eta"],
                             o["alpha"], o["d_min"], o["tangent_max"], o["calib_cond_max"],
-                            int(o["damping_candidates"]), 0 if o["refine"] else 1)
+                            int(o["damping_candidates"]), 1 if o["refine"] else 0)
 
     def _inputs(self, poses, disps, intr, flow, prior, prior_mask, prior_weight=None):
         dev = self.device

@@ -25,13 +25,8 @@ lines.append('| kernel | launches | total us | avg us | ran | avg us (ran) | sha
 for k, v in sorted(agg.items(), key=lambda x: -x[1][1]):
     ran = f'{v[3]/v[2]:.2f}' if v[2] else '-'
     lines.append(f'| `{k}` | {v[0]} | {v[1]:.1f} | {v[1]/v[0]:.2f} | {v[2]} | {ran} | {v[1]/tot:.3f} |')
-want = ['gpu__time_duration.sum', 'dram__bytes_read.sum', 'dram__bytes_write.sum',
-        'gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed', 'sm__throughput.avg.pct_of_peak_sustained_elapsed',
-        'smsp__issue_active.avg.pct_of_peak_sustained_active', 'sm__warps_active.avg.pct_of_peak_sustained_active',
-        'sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active', 'sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active',
-        'sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active',
-        'launch__registers_per_thread', 'launch__grid_size', 'launch__block_size', 'launch__shared_mem_per_block_dynamic',
-        'smsp__inst_executed.sum', 'l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum']
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+from ncu_metrics import WANT as want  # noqa: E402
 res = {}
 for rep in ('pass', 'solve', 'energy'):
     raw = subprocess.run(['ncu', '-i', f'{g}/{rep}_{tag}.ncu-rep', '--page', 'raw', '--csv'], capture_output=True, text=True).stdout

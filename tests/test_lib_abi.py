@@ -99,7 +99,7 @@ int main(void) {
          sizeof(dba_buffers), sizeof(dba_report), sizeof(dba_plan_info), sizeof(dba_stats));
   printf("%zu %zu %zu %zu %zu\n", offsetof(dba_report, energy_trace), offsetof(dba_buffers, nccl_comm),
          offsetof(dba_options, calib_cond_max), offsetof(dba_options, damping_candidates),
-         offsetof(dba_options, no_refine));
+         offsetof(dba_options, refine));
   return 0;
 }'''
     with tempfile.TemporaryDirectory() as d:
@@ -115,4 +115,4 @@ int main(void) {
     assert sizes[7] == _lib.Buffers.nccl_comm.offset
     assert sizes[8] == _lib.Options.calib_cond_max.offset
     assert sizes[9] == _lib.Options.damping_candidates.offset
-    assert sizes[10] == _lib.Options.no_refine.offset
+    assert sizes[10] == _lib.Options.refine.offset
