@@ -55,7 +55,7 @@ constexpr int kPassCTA = kGemmThreads + kPassThreads;
 constexpr int kMaxSlots = 4;  // U-ring depth limit (named barriers 2..9)
 constexpr int kBarGeo = 1, kBarFull = 2, kBarEmpty = 2 + kMaxSlots;
 // register split between the roles (setmaxnreg; 128 * R_gemm + 256 * R_geo <= 384 * 168)
-__host__ __device__ constexpr int pass_gemm_regs(int qmax) { return qmax <= 3 ? 96 : qmax <= 4 ? 112 : 160; }
+__host__ __device__ constexpr int pass_gemm_regs(int qmax) { return qmax <= 3 ? 120 : qmax <= 4 ? 128 : 160; }
 __host__ __device__ constexpr int pass_geo_regs(int qmax) {
   return ((384 * 168 - 128 * pass_gemm_regs(qmax)) / 256) & ~7;
 }
@@ -200,10 +200,10 @@ __host__ __device__ inline PassSmem pass_smem_layout(int kmax, bool calib, int s
   PassSmem s;
   size_t o = 0;
   const int nparts = calib ? 6 : 2;  // phase B: C, gd (+ E_theta x4)
-  s.fbuf = o; o += sizeof(float4) * (size_t)kmax * sub;
+  s.fbuf = o; o += 2 * sizeof(float4) * (size_t)kmax * sub;  // double-buffered: tile t+1 lands under tile t
   s.U = o; o += nslot * sizeof(double) * (size_t)pass_mpad(kmax, calib) * pass_ustride(sub);  // tile ring
   s.parts = o; o += sizeof(double) * (size_t)nparts * kmax * sub;
-  s.dcs = o; o += sizeof(double) * sub;
+  s.dcs = o; o += 2 * sizeof(double) * sub;
   s.dns = o; o += sizeof(double) * sub;
   s.icv = o; o += nslot * sizeof(double) * sub;
   s.qc = o; o += sizeof(double2) * sub;
@@ -273,29 +273,60 @@ __device__ __forceinline__ void gemm_shape(double (&macc)[QMAX][4][2], const dou
                                            const int (&fo_r)[QMAX], const int (&fo_c)[QMAX]) {
   constexpr int kRB = 8 * US;
   constexpr int nks = (US - 4) / 4;
+  constexpr int NI = NC + ND;
+  // fragments of k-step ks + 1 are loaded while the DMMAs of ks issue (explicit double
+  // buffering: the LDS -> DMUL -> DMMA chain of one k-step would otherwise serialise)
+  double ic = icl[0], r0[NI > 0 ? NI : 1], r1[NI > 0 ? NI : 1], c0[NC > 0 ? NC : 1], c1[NC > 0 ? NC : 1];
+#pragma unroll
+  for (int i = 0; i < NI; ++i) {
+    r0[i] = Ub[fo_r[i]];
+    r1[i] = Ub[fo_r[i] + kRB];
+  }
+#pragma unroll
+  for (int i = 0; i < NC; ++i) {
+    c0[i] = Ub[fo_c[i]];
+    c1[i] = Ub[fo_c[i] + kRB];
+  }
 #pragma unroll 2
   for (int ks = 0; ks < nks; ++ks) {
-    const int p0 = 4 * ks;
-    const double ic = icl[p0];
+    const int pn = 4 * (ks + 1 < nks ? ks + 1 : ks);
+    const double icn = icl[pn];
+    double r0n[NI > 0 ? NI : 1], r1n[NI > 0 ? NI : 1], c0n[NC > 0 ? NC : 1], c1n[NC > 0 ? NC : 1];
+#pragma unroll
+    for (int i = 0; i < NI; ++i) {
+      r0n[i] = Ub[fo_r[i] + pn];
+      r1n[i] = Ub[fo_r[i] + kRB + pn];
+    }
 #pragma unroll
     for (int i = 0; i < NC; ++i) {
-      const double* pr = Ub + fo_r[i] + p0;
-      const double* pc = Ub + fo_c[i] + p0;
-      const double a0 = pr[0] * ic, a1 = pr[kRB] * ic;
-      const double c0 = pc[0], c1 = pc[kRB];
-      dmma884(macc[i][0], a0, c0);
-      dmma884(macc[i][1], a0, c1);
-      dmma884(macc[i][2], a1, c0);
-      dmma884(macc[i][3], a1, c1);
+      c0n[i] = Ub[fo_c[i] + pn];
+      c1n[i] = Ub[fo_c[i] + kRB + pn];
+    }
+#pragma unroll
+    for (int i = 0; i < NC; ++i) {
+      const double a0 = r0[i] * ic, a1 = r1[i] * ic;
+      dmma884(macc[i][0], a0, c0[i]);
+      dmma884(macc[i][1], a0, c1[i]);
+      dmma884(macc[i][2], a1, c0[i]);
+      dmma884(macc[i][3], a1, c1[i]);
     }
 #pragma unroll
     for (int j = 0; j < ND; ++j) {
-      const double* pr = Ub + fo_r[NC + j] + p0;
-      const double r0 = pr[0], r1 = pr[kRB];
-      const double a0 = r0 * ic;
-      dmma884(macc[NC + j][0], a0, r0);
-      dmma884(macc[NC + j][1], a0, r1);
-      dmma884(macc[NC + j][3], r1 * ic, r1);
+      const double a0 = r0[NC + j] * ic;
+      dmma884(macc[NC + j][0], a0, r0[NC + j]);
+      dmma884(macc[NC + j][1], a0, r1[NC + j]);
+      dmma884(macc[NC + j][3], r1[NC + j] * ic, r1[NC + j]);
+    }
+    ic = icn;
+#pragma unroll
+    for (int i = 0; i < NI; ++i) {
+      r0[i] = r0n[i];
+      r1[i] = r1n[i];
+    }
+#pragma unroll
+    for (int i = 0; i < NC; ++i) {
+      c0[i] = c0n[i];
+      c1[i] = c1n[i];
     }
   }
 }
@@ -338,7 +369,7 @@ __global__ void __launch_bounds__(kPassCTA, 1) pass_kernel(const PassArgs A) {
   constexpr int SL = SUB / kSlice, US = pass_ustride(SUB);
   const int NS = A.nslot;
   const PassSmem L = pass_smem_layout(A.kmax, CALIB, SUB, NS);
-  float4* fbuf = reinterpret_cast<float4*>(smem + L.fbuf);  // [k][SUB] flow records
+  float4* const fbufb = reinterpret_cast<float4*>(smem + L.fbuf);  // 2 x [k][SUB] flow records
   double* const Ubuf = reinterpret_cast<double*>(smem + L.U);  // U ring: two [mpad][US] slots
   const int ulen = pass_mpad(A.kmax, CALIB) * US;
   double* const icvb = reinterpret_cast<double*>(smem + L.icv);  // 1 / C_p, per ring slot
@@ -484,7 +515,7 @@ __global__ void __launch_bounds__(kPassCTA, 1) pass_kernel(const PassArgs A) {
   // ================================================================ linearisation warps
   asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(pass_geo_regs(QMAX)));
   double* parts = reinterpret_cast<double*>(smem + L.parts);
-  double* dcs = reinterpret_cast<double*>(smem + L.dcs);
+  double* const dcsb = reinterpret_cast<double*>(smem + L.dcs);  // 2 x [SUB]
   double* dns = reinterpret_cast<double*>(smem + L.dns);
   double2* qcs = reinterpret_cast<double2*>(smem + L.qc);  // normalised pixel rays at x_c
   double2* qns = reinterpret_cast<double2*>(smem + L.qn);  // ... at x_n
@@ -559,7 +590,9 @@ __global__ void __launch_bounds__(kPassCTA, 1) pass_kernel(const PassArgs A) {
 
     // cp.async staging of a tile's flow records (16 B each) and disparities;
     // out-of-range pixels are zero-filled
-    auto prefetch = [&](int tile) {
+    auto prefetch = [&](int tile, int buf) {
+      float4* const fbuf = fbufb + buf * KM * SUB;
+      double* const dcs = dcsb + buf * SUB;
       const int pb = tile * SUB;
       for (int x = tid; x < k * SUB; x += kPassThreads) {
         const int a = x / SUB, pl = x - a * SUB, p = pb + pl;
@@ -576,13 +609,15 @@ __global__ void __launch_bounds__(kPassCTA, 1) pass_kernel(const PassArgs A) {
       }
       asm volatile("cp.async.commit_group;");
     };
-    prefetch(A.seg_t0[sg]);
+    prefetch(A.seg_t0[sg], tau & 1);
 
     for (int tile = A.seg_t0[sg]; tile < A.seg_t1[sg]; ++tile, ++tau) {
       const int pbase = tile * SUB;
       const int tb = tau % NS;
       double* const U = Ubuf + tb * ulen;  // this tile's ring slot
       double* const icv = icvb + tb * SUB;
+      const float4* const fbuf = fbufb + (tau & 1) * KM * SUB;
+      const double* const dcs = dcsb + (tau & 1) * SUB;
       asm volatile("cp.async.wait_all;" ::: "memory");
       for (int x = tid; x < SUB; x += kPassThreads) {
         const int p = pbase + x;
@@ -591,6 +626,9 @@ __global__ void __launch_bounds__(kPassCTA, 1) pass_kernel(const PassArgs A) {
         qns[x] = make_double2((pu - cxn) / fxn, (pv - cyn) / fyn);
       }
       nbar_sync(kBarGeo, kPassThreads);
+      // the next tile's records land in the other buffer under this tile's work (its last
+      // reader, tile t-1, is behind the barrier above)
+      if (tile + 1 < A.seg_t1[sg]) prefetch(tile + 1, (tau + 1) & 1);
       // ------------------------------------------------------------ phase A
       // pixel-major: a half-warp per 16 pixels, the two halves split the edges; the
       // per-pixel sums close with one shuffle, so d_n needs no block barrier
@@ -752,7 +790,6 @@ __global__ void __launch_bounds__(kPassCTA, 1) pass_kernel(const PassArgs A) {
         }
       }
       nbar_sync(kBarGeo, kPassThreads);
-      if (tile + 1 < A.seg_t1[sg]) prefetch(tile + 1);  // overlaps the rest of the tile
       // ------------------------------------------------------------ per pixel
       // C_p, g_d,p (+ Eq. 4 prior), 1/C_p and the extra columns; the 1/C_p scaling is
       // applied to the A fragments of the product (M_ext = sum_p U_p U_p^T / C_p)

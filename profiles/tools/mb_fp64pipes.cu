@@ -52,7 +52,7 @@ int main() {
   double* o;
   cudaMalloc(&o, sizeof(double) * sms * 8 * 1024);
   const int iters = 4096;
-  for (int threads : {256, 512, 1024}) {
+  for (int threads : {128, 256, 512}) {
     const int blocks = sms;
     const double warps = (double)blocks * threads / 32;
     const float tm = run<true, false>(o, blocks, threads, iters);
