@@ -52,6 +52,20 @@ def test_oracle_rotation_is_degenerate():
         O.solve(oracle_state(wl), oracle_problem(wl), O.Options(iters=4, optimize_intrinsics=True))
 
 
+def test_oracle_ac4_focal_recovery():
+    """AC4 pinned on the oracle: from the (H+W)/2 heuristic init (56 vs the true
+    64, 12.5 % off) on a translation-rich trajectory, solve_ba_calib recovers fx, fy within 1 %
+    (a smaller helix than the GPU test, so the CPU suite stays fast)."""
+    wl = small_workload(trajectory="helix", frames=40, keyframes=16, radius=3, height=24, width=32,
+                        focal=32.0)
+    heur = np.array([28.0, 28.0, 16.0, 12.0])  # (H+W)/2 at 24x32 (geometry.py:222-225)
+    st = oracle_state(wl)
+    st.intr = heur.copy()
+    res, rep = O.solve(st, oracle_problem(wl), O.Options(iters=8, optimize_intrinsics=True))
+    assert abs(res.intr[0] - 32.0) / 32.0 < 0.01 and abs(res.intr[1] - 32.0) / 32.0 < 0.01, res.intr
+    assert rep.energy_trace[-1] < 1e-3 * rep.energy_trace[0]
+
+
 def test_oracle_solver_failure_at_max_damping():
     wl = small_workload("C1")
     flow = wl.flow.copy()
