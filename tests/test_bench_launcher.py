@@ -59,3 +59,20 @@ def test_ranks_shard_the_edges_by_source_frame(tmp_path):
         allloc += o["local"]
     assert sorted(allloc) == list(range(len(ii)))  # a disjoint cover of the edge set
     assert np.all(np.diff(bounds) > 0)
+
+
+def test_reference_arm_never_loads_the_library():
+    """--impl reference runs the float64 CPU path only: no libdba_b200 and no CUDA library
+    is mapped into the process (checked on a 10-keyframe graph)."""
+    code = (
+        "import sys, json; sys.argv=['bench.py','--impl','reference','--keyframes','10','--steps','1',"
+        "'--warmup','0']; sys.path.insert(0, %r); import bench; bench.main(); "
+        "maps=open('/proc/self/maps').read(); "
+        "print(json.dumps({'dba': 'libdba_b200' in maps, 'cudart': 'libcudart' in maps or 'libcuda.so' in maps}))"
+        % ROOT)
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [json.loads(x) for x in r.stdout.splitlines() if x.startswith("{")]
+    line, maps = lines[0], lines[-1]
+    assert line["impl"] == "reference" and line["value"] > 0 and line["cpu_baseline"]["kind"] == "port"
+    assert not maps["dba"] and not maps["cudart"], maps
