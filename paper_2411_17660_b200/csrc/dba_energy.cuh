@@ -56,7 +56,7 @@ __host__ __device__ inline size_t energy_smem_bytes(int kmax) {
 }
 
 template <bool CALIB>
-__global__ void __launch_bounds__(kEnergyThreads, 3) energy_kernel(const EnergyArgs A) {
+__global__ void __launch_bounds__(kEnergyThreads, 4) energy_kernel(const EnergyArgs A) {
   pdl_enter();
   if (trial_skipped(A.status)) return;
   extern __shared__ __align__(16) unsigned char smem[];
