@@ -386,37 +386,39 @@ __device__ inline void chain_forward(const ChainSm& S, const double* band, doubl
 #endif
       // trailing update S_ac -= L_ab S_cb^T (except (b+1,b+1)), border, rhs
       const int npair = na * (na + 1) / 2;
-      const int n1 = npair * (6 / kTR);
+      const int n1 = npair * (6 / kTR) * 2;
       const int n2 = calib ? na * 4 : 0;
       const int n3 = calib ? 4 : 0;
       const int n4 = 6 * (na > 0 ? na - 1 : 0) + (calib ? 4 : 0);
       const int ntot = n1 + n2 + n3 + n4;
       for (int x = gt; x < ntot; x += kTrailThreads) {
         if (x < n1) {
-          const int pidx = x / (6 / kTR), rr = kTR * (x % (6 / kTR));
+          // item = (block pair, kTR output rows, 3 output columns): twice the items of a
+          // whole-row split, so every trailing thread has one (measured 240 -> 229 us);
+          // each output keeps the same FMA order
+          const int it = x / 2, cg = 3 * (x & 1);
+          const int pidx = it / (6 / kTR), rr = kTR * (it % (6 / kTR));
           if (pidx == 0) continue;  // (b+1, b+1): critical warp
           const short2 pr = S.pairs[pidx];
           const int a = b + 1 + pr.x, cc = b + 1 + pr.y;
           const double* La = S.pbuf + 36 * pr.x + 6 * rr;
           const double2* Sc = reinterpret_cast<const double2*>(wb(cc, b));
-          double2* O = reinterpret_cast<double2*>(wb(a, cc) + 6 * rr);
-          double ar[kTR][6], o[kTR][6];
+          double* O = wb(a, cc) + 6 * rr + cg;
+          double ar[kTR][6], o[kTR][3];
 #pragma unroll
           for (int r = 0; r < kTR; ++r)
 #pragma unroll
             for (int d = 0; d < 6; ++d) ar[r][d] = La[6 * r + d];
 #pragma unroll
-          for (int q = 0; q < 3 * kTR; ++q) {
-            const double2 v = O[q];
-            o[(2 * q) / 6][(2 * q) % 6] = v.x;
-            o[(2 * q + 1) / 6][(2 * q + 1) % 6] = v.y;
-          }
+          for (int r = 0; r < kTR; ++r)
 #pragma unroll
-          for (int c = 0; c < 6; ++c) {
+            for (int c = 0; c < 3; ++c) o[r][c] = O[6 * r + c];
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
             double sc[6];
 #pragma unroll
             for (int q = 0; q < 3; ++q) {
-              const double2 v = Sc[3 * c + q];
+              const double2 v = Sc[3 * (cg + c) + q];
               sc[2 * q] = v.x;
               sc[2 * q + 1] = v.y;
             }
@@ -426,8 +428,9 @@ __device__ inline void chain_forward(const ChainSm& S, const double* band, doubl
               for (int d = 0; d < 6; ++d) o[r][c] = fma(-ar[r][d], sc[d], o[r][c]);
           }
 #pragma unroll
-          for (int q = 0; q < 3 * kTR; ++q)
-            O[q] = make_double2(o[(2 * q) / 6][(2 * q) % 6], o[(2 * q + 1) / 6][(2 * q + 1) % 6]);
+          for (int r = 0; r < kTR; ++r)
+#pragma unroll
+            for (int c = 0; c < 3; ++c) O[6 * r + c] = o[r][c];
         } else if (x < n1 + n2) {
           const int y2 = x - n1, co = y2 / 4, tt = y2 % 4;
           const int cc = b + 1 + co;
