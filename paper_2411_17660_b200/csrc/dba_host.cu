@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <climits>
@@ -1582,7 +1583,17 @@ int gauge_sum(Ctx& c, const float* d, double* out) {
 
 extern "C" {
 
+// NVTX ranges (header-only NVTX3: free without an attached profiler) around the host
+// phases of a solve, so an Nsight Systems timeline groups each call's launches
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
 int dba_solve(dba_plan* p, const dba_options* o, const dba_buffers* b, dba_report* rep) {
+  NvtxRange nv_call("dba_solve");
   int s = check_args(p, o, b);
   if (s) return s;
   if (!rep || !b->poses_out || !b->disps_out || !b->intr_out) return DBA_EINVAL;
@@ -1596,7 +1607,10 @@ int dba_solve(dba_plan* p, const dba_options* o, const dba_buffers* b, dba_repor
   double* gsum = c.at<double>(p->L.gauge);
   if (p->gauge_on)
     if ((s = gauge_sum(c, b->disps_in, gsum))) return rep->status = s;
-  if ((s = initial_pass(c))) return rep->status = s;
+  {
+    NvtxRange nv("dba_initial_linearisation");
+    if ((s = initial_pass(c))) return rep->status = s;
+  }
   Readback rb;
   if ((s = read_flags(c, 0, rb))) return rep->status = s;
   if (rb.status[1] != INT_MAX || !std::isfinite(rb.energy)) {
@@ -1628,8 +1642,10 @@ int dba_solve(dba_plan* p, const dba_options* o, const dba_buffers* b, dba_repor
                         (long long)ctl.lins * lg.nodes_lin;
   }
   for (int seen = 0; !graphed && o->iters > 0;) {
+    NvtxRange nv_batch("dba_lm_batch");
     const int batch = std::max(1, o->iters - seen);
     for (int t = 0; t < batch; ++t) {
+      NvtxRange nv_round("dba_lm_round");
       // round: the reduced system is factored for nspec damping values at once
       // (lambda, 10 lambda, ... -- the trials successive rejections would run); then,
       // per candidate in order, step + energy-only pass (back-substitution and
