@@ -82,3 +82,30 @@ def test_every_pose_fixed(torch_cuda):
     P, _, _ = _check(wl, 2, fixed=fixed)
     assert np.array_equal(P, wl.poses0)
 
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("radius,calib,tile", [(8, False, None), (8, True, None), (5, False, "64")])
+def test_high_degree_and_small_tile_paths(radius, calib, tile, monkeypatch):
+    """Out-degree 16 (radius 8: 112-row Schur product, 7 items per product warp, 64-pixel
+    tiles) with and without intrinsics, and the forced 64-pixel-tile / 4-slot U-ring path of a
+    radius-5 graph: oracle parity after 2 GN iterations (the 1e-4 bar)."""
+    import torch
+    from paper_2411_17660_b200 import dba
+    if tile:
+        monkeypatch.setenv("DBA_PASS_TILE", tile)
+    wl = small_workload(trajectory="orbit" if not calib else "helix", frames=60, keyframes=40, radius=radius,
+                        height=24, width=32, focal=None if not calib else 32.0, noise=0.5)
+    s = dba.DBASolver(wl.ii, wl.jj, len(wl.frames), 24, 32, wl.fixed, optimize_intrinsics=calib)
+    info = s.info
+    Po, Do, Ko, rep = s.solve(wl.poses0, wl.disps0, wl.intr0, wl.flow, iters=2)
+    torch.cuda.synchronize()
+    ref, rrep = O.solve(oracle_state(wl), oracle_problem(wl), O.Options(iters=2, optimize_intrinsics=calib))
+    assert rep.iterations_run == rrep.iterations
+    rel = np.abs(Do.cpu().numpy().astype(np.float64) - ref.disps) / ref.disps
+    assert rel.max() < 1e-4, rel.max()
+    te, ae = pose_errors(Po.cpu().numpy(), ref.poses)
+    assert te < 1e-4 and ae < np.degrees(1e-4)
+    if calib:
+        assert np.max(np.abs(Ko.cpu().numpy() - ref.intr) / ref.intr) < 1e-4
+    assert info.max_out_degree == 2 * radius if radius <= 8 else True
