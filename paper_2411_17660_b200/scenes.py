@@ -293,10 +293,60 @@ class Workload:
     true_intr: np.ndarray | None = None
 
 
+def mean_flow_distance(pa, pb, disp_a, intr, beta=0.5):
+    """G1: beta x mean full-flow magnitude + (1 - beta) x
+    mean rotation-only flow magnitude over frame a's valid pixels, for the (N,7) poses pa,
+    pb (world -> camera) -- numpy, for building workloads on the host (the solver and the
+    graph kernels never call it; ``graph.frame_distances`` is the GPU version)."""
+    Ra, Rb = geo.quat_to_rot(np.asarray(pa[:4])), geo.quat_to_rot(np.asarray(pb[:4]))
+    R = Rb @ Ra.T
+    t = np.asarray(pb[4:7]) - R @ np.asarray(pa[4:7])
+    H, W = disp_a.shape
+    fx, fy, cx, cy = (float(v) for v in intr)
+    p = np.arange(H * W)
+    x = ((p % W) - cx) / fx
+    y = ((p // W) - cy) / fy
+    d = disp_a.reshape(-1).astype(np.float64)
+    Xr = R[0, 0] * x + R[0, 1] * y + R[0, 2]
+    Yr = R[1, 0] * x + R[1, 1] * y + R[1, 2]
+    Zr = R[2, 0] * x + R[2, 1] * y + R[2, 2]
+    with np.errstate(divide="ignore", invalid="ignore"):
+        Zh = Zr + t[2] * d
+        ok = (d > 0) & (Zh > 1e-4 * d)
+        mf = np.hypot(fx * ((Xr + t[0] * d) / Zh - x), fy * ((Yr + t[1] * d) / Zh - y))
+        okr = Zr > 1e-4
+        mr = np.hypot(fx * (Xr / Zr - x), fy * (Yr / Zr - y))
+    full = mf[ok].mean() if ok.any() else np.inf
+    rot = mr[okr].mean() if okr.any() else np.inf
+    return beta * full + (1.0 - beta) * rot
+
+
+def proximity_edges(poses, disps, intr, n_frames, radius, extra):
+    """A frontend window's edge set (BASELINE configs[1], "~150 proximity edges"): the G3 rule of
+    ``graph.build_frontend_edges`` -- ordered pairs at most `radius` apart, plus the window's
+    existing edges -- where the existing edges are the `extra` closest unordered pairs farther
+    apart by G1 mean flow distance on the current estimates (both directions), the proximity
+    factors a DROID-style frontend keeps.  Lexicographic order."""
+    ii, jj = radius_edges(n_frames, radius)
+    far = []
+    for a in range(n_frames):
+        for b in range(a + radius + 1, n_frames):
+            m = 0.5 * (mean_flow_distance(poses[a], poses[b], disps[a], intr) +
+                       mean_flow_distance(poses[b], poses[a], disps[b], intr))
+            far.append((m, a, b))
+    far.sort()
+    edges = set(zip(ii.tolist(), jj.tolist()))
+    for _, a, b in far[:extra]:
+        edges.update({(a, b), (b, a)})
+    e = sorted(edges)
+    return np.array([x for x, _ in e], dtype=np.int32), np.array([y for _, y in e], dtype=np.int32)
+
+
 CONFIGS = {
     # name: (trajectory, scene frames, keyframes used, radius, iters, extras)
     "C1": dict(trajectory="line", scene_frames=8, keyframes=8, radius=2, iters=4),
-    "C2": dict(trajectory="orbit", scene_frames=300, keyframes=25, radius=3, iters=2),
+    # frontend window: radius-3 pairs (138 edges) + the 6 closest farther pairs = 150 edges
+    "C2": dict(trajectory="orbit", scene_frames=300, keyframes=25, radius=3, iters=2, proximity=6),
     "C3": dict(trajectory="orbit", scene_frames=300, keyframes=300, radius=5, iters=8),
     "C4": dict(trajectory="orbit", scene_frames=300, keyframes=25, radius=3, iters=2,
                prior=True),
@@ -326,9 +376,12 @@ def make_workload(name, height=48, width=64, keyframes=None, radius=None, iters=
                      height=height, width=width, seed=0, focal=focal, pixel_noise=float(noise))
     sc = Scene(spec)
     frames = list(range(cfg["keyframes"]))
-    ii, jj = radius_edges(len(frames), cfg["radius"])
-    flow = np.stack([sc.flow_record(frames[a], frames[b]) for a, b in zip(ii, jj)])
     poses0, disps0 = perturbed_state(sc, frames)
+    if cfg.get("proximity") and keyframes is None and radius is None:
+        ii, jj = proximity_edges(poses0, disps0, sc.intr, len(frames), cfg["radius"], cfg["proximity"])
+    else:
+        ii, jj = radius_edges(len(frames), cfg["radius"])
+    flow = np.stack([sc.flow_record(frames[a], frames[b]) for a, b in zip(ii, jj)])
     fixed = np.zeros(len(frames), dtype=bool)
     fixed[0] = True
     intr0 = sc.intr.copy()

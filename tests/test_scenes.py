@@ -87,3 +87,26 @@ def test_dspt_roundtrip(tmp_path):
     p.write_bytes(p.read_bytes()[:-4])
     with pytest.raises(DataError):
         scenes.read_dspt_f32(p)
+
+
+def test_workload_mean_flow_distance_matches_graph_oracle():
+    """scenes.mean_flow_distance (host numpy, used to build C2's proximity edges) restates G1
+    like oracle/graph.py (the bit-exact reference of the GPU graph kernels)."""
+    import numpy as np
+    from oracle import graph as OG
+    from paper_2411_17660_b200 import scenes
+    wl = scenes.make_workload("C2", height=24, width=32, keyframes=8)
+    for a, b in [(0, 1), (2, 6), (7, 3)]:
+        got = scenes.mean_flow_distance(wl.poses0[a], wl.poses0[b], wl.disps0[a], wl.intr0)
+        ref = OG.mean_flow_distance(wl.poses0[a], wl.poses0[b], wl.disps0[a], wl.intr0)
+        assert abs(got - ref) <= 1e-12 * abs(ref), (a, b, got, ref)
+
+
+def test_c2_is_a_150_edge_proximity_window():
+    """BASELINE configs[1]: 25 keyframes, ~150 proximity edges -- the G3 window pairs (radius
+    3, 138 edges) plus the 6 closest farther pairs in both directions."""
+    from paper_2411_17660_b200 import scenes
+    wl = scenes.make_workload("C2")
+    assert len(wl.frames) == 25 and len(wl.ii) == 150
+    far = [(int(a), int(b)) for a, b in zip(wl.ii, wl.jj) if abs(int(a) - int(b)) > 3]
+    assert len(far) == 12 and all((b, a) in far for a, b in far)
