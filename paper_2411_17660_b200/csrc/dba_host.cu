@@ -484,14 +484,13 @@ int dba_plan_create(const dba_problem_desc* d, dba_plan** out) {
       }
     }
     p->pass_smem = s.total;
-    // product items per product warp (pass_quads): 3 up to 64 GEMM rows (radius-5
-    // graphs), 4 up to 80 (with intrinsics), 7 up to 112 (out-degree 16)
-    // (the finer split only where it needs no more items per warp)
+    // product items per product warp (pass_quads, 8 warps): 2 up to 80 GEMM rows (radius-5
+    // graphs, with or without intrinsics), 3 up to 96, 4 up to 112 (out-degree 16)
     const int np = pass_mpad(std::max(p->kmax, 1), p->calib) >> 4;
-    p->split = pass_qmax(np, true) <= pass_qmax(np, false) ? 1 : 0;
-    const int qm = pass_qmax(np, p->split != 0);
-    p->mb = qm <= 3 ? 3 : qm <= 4 ? 4 : 7;
-    if (p->pass_smem > 225 * 1024 || qm > 7) {
+    p->split = 0;  // the compile-time product shapes (gemm_dispatch) are for unsplit items
+    const int qm = pass_qmax(np, false);
+    p->mb = qm <= 2 ? 2 : qm <= 3 ? 3 : 4;
+    if (p->pass_smem > 225 * 1024 || qm > 4) {
       delete p;
       return DBA_ECAPACITY;
     }
@@ -1117,10 +1116,10 @@ int launch_pass(Ctx& c, int cur, int nxt, bool backsub, bool system, bool gated 
   a.seg_off_M = c.at<long long>(p->L.seg_off_M);
   a.seg_off_w = c.at<long long>(p->L.seg_off_w);
   if (p->calib)
-    return p->mb == 3 ? launch_pass_t<true, 3>(c, a) : p->mb == 4 ? launch_pass_t<true, 4>(c, a)
-                                                             : launch_pass_t<true, 7>(c, a);
-  return p->mb == 3 ? launch_pass_t<false, 3>(c, a) : p->mb == 4 ? launch_pass_t<false, 4>(c, a)
-                                                            : launch_pass_t<false, 7>(c, a);
+    return p->mb == 2 ? launch_pass_t<true, 2>(c, a) : p->mb == 3 ? launch_pass_t<true, 3>(c, a)
+                                                             : launch_pass_t<true, 4>(c, a);
+  return p->mb == 2 ? launch_pass_t<false, 2>(c, a) : p->mb == 3 ? launch_pass_t<false, 3>(c, a)
+                                                            : launch_pass_t<false, 4>(c, a);
 }
 
 // LM controller inputs: the trial (slot 1) energy, the flags word and the options

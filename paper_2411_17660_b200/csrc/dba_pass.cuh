@@ -47,17 +47,19 @@ namespace dba {
 
 constexpr int kPassThreads = 256;  // linearisation (geometry) threads
 constexpr int kPassWarps = 8;
-constexpr int kGemmWarps = 4;      // one warpgroup: the tensor-core Schur product
+constexpr int kGemmWarps = 8;      // two warpgroups: the tensor-core Schur product
 constexpr int kGemmThreads = 32 * kGemmWarps;
 constexpr int kPassCTA = kGemmThreads + kPassThreads;
 // named barriers: geometry warps only; U-ring slot b full (geometry -> product warps),
 // slot b empty (product -> geometry)
 constexpr int kMaxSlots = 4;  // U-ring depth limit (named barriers 2..9)
 constexpr int kBarGeo = 1, kBarFull = 2, kBarEmpty = 2 + kMaxSlots;
-// register split between the roles (setmaxnreg; 128 * R_gemm + 256 * R_geo <= 384 * 168)
-__host__ __device__ constexpr int pass_gemm_regs(int qmax) { return qmax <= 3 ? 120 : qmax <= 4 ? 128 : 160; }
+// register split between the roles (setmaxnreg; 256 * R_gemm + 256 * R_geo <= 512 * 128):
+// product warps 72 registers for up to 2 items (measured: 64 spills in the k-loop, 88 costs
+// the linearisation warps theirs), more for the rare high-degree shapes
+__host__ __device__ constexpr int pass_gemm_regs(int qmax) { return qmax <= 2 ? 72 : qmax <= 3 ? 80 : 96; }
 __host__ __device__ constexpr int pass_geo_regs(int qmax) {
-  return ((384 * 168 - 128 * pass_gemm_regs(qmax)) / 256) & ~7;
+  return ((kPassCTA * 128 - kGemmThreads * pass_gemm_regs(qmax)) / kPassThreads) & ~7;
 }
 constexpr int kSlice = 32;     // pixels per phase-B edge unit (1 per lane)
 constexpr int kEdgeSlots = 2;  // distinct edges per warp per segment (see pass_units)
@@ -353,12 +355,13 @@ __device__ __forceinline__ void nbar_arrive(int id, int n) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
-// Warp-specialised: warpgroup 0 (kGemmWarps warps) runs the tensor-core product, the
+// Warp-specialised: warpgroups 0-1 (kGemmWarps warps) run the tensor-core product, the
 // other 8 warps the per-pixel linearisation.  Per tile the geometry warps fill U-ring
 // slot b (tile sequence number mod the ring depth) and hand it over (kBarFull + b); the product warps
 // drain it and hand it back (kBarEmpty + b).  DMMA and DFMA share the fp64 datapath
 // (profiles/tools/mb_fp64pipes.cu), so the point is that every SM sub-partition always has
-// a warp with fp64 work ready: one product warp next to two linearisation warps.
+// a warp with fp64 work ready: two product warps next to two linearisation warps (one lone
+// product warp per sub-partition issued a DMMA only every ~32 cycles).
 template <bool CALIB, int QMAX, int SUB>
 __global__ void __launch_bounds__(kPassCTA, 1) pass_kernel(const PassArgs A) {
   pdl_enter();
