@@ -99,7 +99,7 @@ struct dba_plan {
   int calib = 0, prior = 0, freeze_d = 0, gauge_on = 0, gauge_frame = -1, rank = 0, nranks = 1;
   int scalefix = 0, anchor = -1;  // prior-fixed monocular scale: exact-row step correction
   int f0 = 0, f1 = 0, NL = 0, EL = 0, kmax = 0, nb = 0, BW = 0, n_red = 0;
-  int n_tiles = 0, G = 0, nseg = 0, n_units = 0, nve = kEdgeVals, sub = 128, mb = 3, split = 0, nslot = 2, ring = 32;
+  int n_tiles = 0, G = 0, nseg = 0, n_units = 0, nve = kEdgeVals, sub = 128, mb = 3, nslot = 2, ring = 32;
   size_t pass_smem = 0, solve_smem = 0;
   long long sys_len = 0;  // doubles in one packed reduced system
   long long spec_delta = 0, spec_Lband = 0, spec_rLband = 0, spec_mid = 0;  // per damping candidate
@@ -487,8 +487,7 @@ int dba_plan_create(const dba_problem_desc* d, dba_plan** out) {
     // product items per product warp (pass_quads, 8 warps): 2 up to 80 GEMM rows (radius-5
     // graphs, with or without intrinsics), 3 up to 96, 4 up to 112 (out-degree 16)
     const int np = pass_mpad(std::max(p->kmax, 1), p->calib) >> 4;
-    p->split = 0;  // the compile-time product shapes (gemm_dispatch) are for unsplit items
-    const int qm = pass_qmax(np, false);
+    const int qm = pass_qmax(np);
     p->mb = qm <= 2 ? 2 : qm <= 3 ? 3 : 4;
     if (p->pass_smem > 225 * 1024 || qm > 4) {
       delete p;
@@ -1078,7 +1077,6 @@ int launch_pass(Ctx& c, int cur, int nxt, bool backsub, bool system, bool gated 
   a.n_tiles = p->n_tiles;
   a.kmax = std::max(p->kmax, 1);
   a.sub = p->sub;
-  a.split = p->split;
   a.nslot = p->nslot;
   a.backsub = backsub ? 1 : 0;
   (void)system;

@@ -66,7 +66,6 @@ constexpr int kEdgeSlots = 2;  // distinct edges per warp per segment (see pass_
 
 struct PassArgs {
   int H, W, P, n_tiles, kmax, sub;
-  int split;    // product item split (pass_quads)
   int nslot;    // U-ring depth (2..kMaxSlots)
   int backsub;  // run phase A
   int freeze;   // disparity block frozen (motion-only / pose stage): no Schur fill-in, d unchanged
@@ -128,32 +127,29 @@ __host__ __device__ inline int pass_mpad(int k, bool calib) { return (pass_mext(
 __host__ __device__ constexpr int pass_ustride(int sub) { return sub + 4; }
 
 // Work split of the symmetric product M_ext = V C^-1 V^T (upper triangle, 8x8 blocks).
-// The np = mpad/16 row PAIRS of blocks give three kinds of items:
+// The np = mpad/16 row PAIRS of blocks give two kinds of items:
 //   cross (r < c): the 2x2 block square {2r, 2r+1} x {2c, 2c+1}: 4 fragments, 4 DMMAs
-//   dpair (r = c): the diagonal blocks (2r,2r), (2r+1,2r+1): 2 fragments, 2 DMMAs
-//   doff  (r = c): the block (2r, 2r+1): 2 fragments, 1 DMMA
+//   diag  (r = c): (2r,2r), (2r,2r+1), (2r+1,2r+1): 2 fragments, 3 DMMAs
 // (A and B fragments of one block row are the same shared-memory words.)  Items go to
 // the kGemmWarps product warps longest-first onto the least-loaded warp, lowest index on
-// ties (np = 4, radius-5 graphs, unsplit: 8, 8, 10, 10 DMMAs per k-step; split: 9 each
-// but 4 items on some warps, i.e. more accumulator registers).  Without `split` a diagonal pair is
-// one item, (2r,2r), (2r,2r+1), (2r+1,2r+1) (kind 3: 2 fragments, 3 DMMAs): fewer items
-// per warp (registers) at a coarser balance.  Every thread evaluates the same
-// deterministic assignment.  Returns the number of items of warp `w`, their pairs and
-// kinds (0 cross, 1 dpair, 2 doff, 3 diag) in (qr, qc, qk) when non-null.
+// ties (np = 4, radius-5 graphs: 4,4,4,4,4,4,6,6 DMMAs per k-step; splitting the diagonal
+// items for an exact balance measured no faster and needs more accumulator registers).
+// Every thread evaluates the same deterministic assignment.  Returns the number of items
+// of warp `w`, their pairs and kinds (0 cross, 3 diag) in (qr, qc, qk) when non-null.
 template <int QMAX>
-__host__ __device__ inline int pass_quads(int np, int w, bool split, int* qr, int* qc, int* qk) {
+__host__ __device__ inline int pass_quads(int np, int w, int* qr, int* qc, int* qk) {
   constexpr int nw = kGemmWarps;
   int load[nw];
   for (int x = 0; x < nw; ++x) load[x] = 0;
   int n = 0;
-  for (int kind = 0; kind < 4; ++kind)
+  for (int kind = 0; kind < 4; kind += 3)
     for (int r = 0; r < np; ++r)
       for (int c = r; c < np; ++c) {
-        if ((kind == 0) != (r < c) || (kind == 3 && split) || ((kind == 1 || kind == 2) && !split)) continue;
+        if ((kind == 0) != (r < c)) continue;
         int best = 0;
         for (int x = 1; x < nw; ++x)
           if (load[x] < load[best]) best = x;
-        load[best] += kind == 0 ? 4 : kind == 1 ? 2 : kind == 2 ? 1 : 3;
+        load[best] += kind == 0 ? 4 : 3;
         if (best == w) {
           if (qr) {
 #pragma unroll
@@ -170,10 +166,10 @@ __host__ __device__ inline int pass_quads(int np, int w, bool split, int* qr, in
   return n;
 }
 // largest per-warp item count for np row pairs (the plan picks QMAX from it)
-__host__ __device__ inline int pass_qmax(int np, bool split) {
+__host__ __device__ inline int pass_qmax(int np) {
   int m = 0;
   for (int w = 0; w < kGemmWarps; ++w) {
-    const int n = pass_quads<1>(np, w, split, nullptr, nullptr, nullptr);
+    const int n = pass_quads<1>(np, w, nullptr, nullptr, nullptr);
     m = n > m ? n : m;
   }
   return m;
@@ -398,7 +394,7 @@ __global__ void __launch_bounds__(kPassCTA, 1) pass_kernel(const PassArgs A) {
       int qr[QMAX], qc[QMAX], qk[QMAX];
 #pragma unroll
       for (int q = 0; q < QMAX; ++q) qr[q] = qc[q] = qk[q] = 0;
-      const int nq = pass_quads<QMAX>(np, warp, A.split != 0, qr, qc, qk);
+      const int nq = pass_quads<QMAX>(np, warp, qr, qc, qk);
       const int lane_off = (lane >> 2) * US + (lane & 3);
       int fo_r[QMAX], fo_c[QMAX];
 #pragma unroll
@@ -421,23 +417,14 @@ __global__ void __launch_bounds__(kPassCTA, 1) pass_kernel(const PassArgs A) {
       for (int q = 0; q < QMAX; ++q) nc += (q < nq && qk[q] == 0) ? 1 : 0;
       auto gemm = [&](const double* Ub, const double* ic_b) {
         const double* icl = ic_b + (lane & 3);
-        if (QMAX <= 4 && !A.split && gemm_dispatch<QMAX, US, 0, 0>(nc, nq - nc, macc, Ub, icl, fo_r, fo_c))
+        if (QMAX <= 4 && gemm_dispatch<QMAX, US, 0, 0>(nc, nq - nc, macc, Ub, icl, fo_r, fo_c))
           return;
         // generic: item by item, branch-free unrolled k-loops per item
 #pragma unroll
         for (int q = 0; q < QMAX; ++q) {
           if (q >= nq) break;
           const double* pr = Ub + fo_r[q];
-          if (qk[q] == 1) {  // (2r,2r), (2r+1,2r+1)
-#pragma unroll 4
-            for (int ks = 0; ks < nks; ++ks) {
-              const int p0 = 4 * ks;
-              const double ic = icl[p0];
-              const double b0 = pr[p0], b1 = pr[kRB + p0];
-              dmma884(macc[q][0], b0 * ic, b0);
-              dmma884(macc[q][3], b1 * ic, b1);
-            }
-          } else if (qk[q] == 3) {  // (2r,2r), (2r,2r+1), (2r+1,2r+1)
+          if (qk[q] == 3) {  // (2r,2r), (2r,2r+1), (2r+1,2r+1)
 #pragma unroll 4
             for (int ks = 0; ks < nks; ++ks) {
               const int p0 = 4 * ks;
@@ -447,13 +434,6 @@ __global__ void __launch_bounds__(kPassCTA, 1) pass_kernel(const PassArgs A) {
               dmma884(macc[q][0], a0, b0);
               dmma884(macc[q][1], a0, b1);
               dmma884(macc[q][3], b1 * ic, b1);
-            }
-          } else if (qk[q] == 2) {  // (2r, 2r+1)
-#pragma unroll 4
-            for (int ks = 0; ks < nks; ++ks) {
-              const int p0 = 4 * ks;
-              const double ic = icl[p0];
-              dmma884(macc[q][1], pr[p0] * ic, pr[kRB + p0]);
             }
           } else {
             const double* pc = Ub + fo_c[q];
@@ -486,10 +466,8 @@ __global__ void __launch_bounds__(kPassCTA, 1) pass_kernel(const PassArgs A) {
       if (q >= nq) continue;
 #pragma unroll
       for (int b = 0; b < 4; ++b) {
-        // blocks of the item: cross all four, dpair 0 and 3, doff 1, diag 0, 1 and 3
-        if (qk[q] == 1 && (b == 1 || b == 2)) continue;
+        // blocks of the item: cross all four, diag 0, 1 and 3
         if (qk[q] == 3 && b == 2) continue;
-        if (qk[q] == 2 && b != 1) continue;
         const int bi = 2 * qr[q] + (b >> 1), bj = 2 * qc[q] + (b & 1);
 #pragma unroll
         for (int i = 0; i < 2; ++i) {
