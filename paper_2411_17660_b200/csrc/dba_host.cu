@@ -503,16 +503,21 @@ int dba_plan_create(const dba_problem_desc* d, dba_plan** out) {
   p->device = dev;
   const long long items = (long long)p->NL * p->n_tiles;
   p->G = (int)std::max<long long>(1, std::min<long long>(items, (long long)sms));  // one 512-thread CTA per SM
-  // weighted contiguous split, cost of a tile ~ (out-degree + 2)
+  // weighted contiguous split; the cost of a tile of a frame with out-degree k, fitted to
+  // per-CTA pass times on C3 (profiles/tools/pass_balance.py: 2.88 + 0.10 k + 0.095 D us,
+  // D = DMMAs per k-step of the padded product; a segment boundary costs < 0.5 us)
   std::vector<int> seg_frame, seg_t0, seg_t1, cta_seg(p->G + 1, 0), frame_seg(p->NL + 1, 0);
   {
+    auto tile_cost = [&](int k) -> long long {
+      const int np = pass_mpad(std::max(k, 1), p->calib) >> 4;
+      return 2880 + 100LL * k + 95LL * (2 * np * (np - 1) + 3 * np);
+    };
     long long tot = 0;
-    for (int fl = 0; fl < p->NL; ++fl)
-      tot += (long long)(csr_off[fl + 1] - csr_off[fl] + 2) * p->n_tiles;
+    for (int fl = 0; fl < p->NL; ++fl) tot += tile_cost(csr_off[fl + 1] - csr_off[fl]) * p->n_tiles;
     long long cum = 0;
     int cur_cta = -1, cur_fl = -1;
     for (int fl = 0; fl < p->NL; ++fl) {
-      const long long c = csr_off[fl + 1] - csr_off[fl] + 2;
+      const long long c = tile_cost(csr_off[fl + 1] - csr_off[fl]);
       for (int t = 0; t < p->n_tiles; ++t) {
         int cta = (int)std::min<long long>(p->G - 1, ((2 * cum + c) * p->G) / (2 * std::max(tot, 1LL)));
         cta = std::max(cta, std::max(cur_cta, 0));
@@ -1879,3 +1884,15 @@ int dba_nccl_comm_destroy(void* comm) {
 }
 
 }  // extern "C"
+
+#ifdef DBA_PASS_TIMING
+// diagnostic build only (profiles/tools/pass_balance.py): per-CTA pass timestamps
+// (entry, last product warp, last linearisation warp; globaltimer ns; SM id), then reset
+extern "C" int dba_debug_pass_times(unsigned long long* out, int n) {
+  n = std::min(n, 4 * 1024);
+  if (out && cudaMemcpyFromSymbol(out, dba::g_pass_t, sizeof(unsigned long long) * n) != cudaSuccess)
+    return DBA_ECUDA;
+  static unsigned long long zero[4 * 1024] = {};
+  return cudaMemcpyToSymbol(dba::g_pass_t, zero, sizeof(zero)) == cudaSuccess ? DBA_OK : DBA_ECUDA;
+}
+#endif

@@ -358,11 +358,37 @@ __device__ __forceinline__ void nbar_arrive(int id, int n) {
 // (profiles/tools/mb_fp64pipes.cu), so the point is that every SM sub-partition always has
 // a warp with fp64 work ready: two product warps next to two linearisation warps (one lone
 // product warp per sub-partition issued a DMMA only every ~32 cycles).
+// DBA_PASS_TIMING (diagnostic build, profiles/tools/pass_balance.py): per CTA the
+// globaltimer at entry and when its last product / linearisation warp finishes, and its SM
+#ifdef DBA_PASS_TIMING
+__device__ unsigned long long g_pass_t[4 * 1024];
+__device__ __forceinline__ unsigned long long pass_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define PASS_T_MARK(slot)                                                                   \
+  do {                                                                                      \
+    if ((threadIdx.x & 31) == 0) atomicMax(&g_pass_t[4 * blockIdx.x + (slot)], pass_now()); \
+  } while (0)
+#else
+#define PASS_T_MARK(slot) \
+  do {                    \
+  } while (0)
+#endif
 template <bool CALIB, int QMAX, int SUB>
 __global__ void __launch_bounds__(kPassCTA, 1) pass_kernel(const PassArgs A) {
   pdl_enter();
   if (trial_skipped(A.status)) return;
   if (A.runs && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(A.runs, 1ull);
+#ifdef DBA_PASS_TIMING
+  if (threadIdx.x == 0) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    g_pass_t[4 * blockIdx.x] = pass_now();
+    g_pass_t[4 * blockIdx.x + 3] = smid;
+  }
+#endif
   extern __shared__ __align__(16) unsigned char smem[];
   constexpr int NVE = kEdgeVals + (CALIB ? kCalibVals : 0);
   constexpr int SL = SUB / kSlice, US = pass_ustride(SUB);
@@ -490,6 +516,7 @@ __global__ void __launch_bounds__(kPassCTA, 1) pass_kernel(const PassArgs A) {
       }
     }
     }  // segments
+    PASS_T_MARK(1);
     return;
   }
 
@@ -859,6 +886,7 @@ __global__ void __launch_bounds__(kPassCTA, 1) pass_kernel(const PassArgs A) {
     }
     nbar_sync(kBarGeo, kPassThreads);
   }  // segments
+  PASS_T_MARK(2);
 }
 
 }  // namespace dba

@@ -4,12 +4,16 @@
 // frame couples the poses {i} U out(i), so with the (free-pose) ordering used
 // by the plan every nonzero 6x6 block (a, c) satisfies |a - c| <= BW.  The
 // intrinsics (4 rows, "global block") form a dense border that is
-// eliminated last.  The band is factored as a block LDL^T,
-//     L_ab = S_ab D_b^-1,   S_ac -= L_ab S_cb^T,   D_b = S_bb (updated),
-// with a sliding window of BW+1 block rows resident in shared memory.  D_b is
-// SPD iff the damped system is; D_b^-1 comes from two 3x3 adjugate inverses
-// (leading-minor test = the Cholesky pivot test).  Damping lambda is added to a
-// diagonal block when it becomes a pivot.
+// eliminated last.  The band is factored as a block Cholesky for the Schur updates and
+// kept in block LDL^T form for the substitutions:
+//     D_b = S_bb (updated) + lambda I = C_b C_b^T,   Li_b = C_b^-1,
+//     W_ab = S_ab Li_b^T,   S_ac -= W_ab W_cb^T,   L_ab = W_ab Li_b,   D_b^-1 = Li_b^T Li_b,
+// with a sliding window of BW+1 block rows resident in shared memory.  The symmetric
+// update W W^T is backward stable: the former L_ab S_cb^T form (explicit D_b^-1 from 3x3
+// adjugates) left the noisy-C3 step 4e-7 from the exact solution against 1e-10 for
+// LAPACK; this form matches LAPACK (numpy emulation).  The Cholesky pivot
+// test (every pivot > 0) is the SPD test.  Damping lambda is added to a diagonal block
+// when it becomes a pivot.
 //
 // The factorisation is a chain of dependent 6x6 pivots, so:
 //  * two-sided (solve2_kernel, cooperative, 2 CTAs): CTA 0 eliminates poses
@@ -108,7 +112,7 @@ __host__ __device__ inline long long solve_mid_len(int BW) {
 }
 
 struct SolveSmem {
-  size_t win, ring, th, thL, z, thm, thLm, zm, dinv, pbuf, cbuf, tbuf, pairs, xo, bars, total;
+  size_t win, ring, th, thL, z, thm, thLm, zm, linv, pbuf, cbuf, tbuf, pairs, xo, bars, total;
 };
 __host__ __device__ inline SolveSmem solve_smem_layout(int nb, int BW, int calib, int ring = kRing) {
   SolveSmem s;
@@ -121,10 +125,10 @@ __host__ __device__ inline SolveSmem solve_smem_layout(int nb, int BW, int calib
   s.thm = o; o += sizeof(double) * (calib ? (size_t)BW * 24 + 16 : 0);
   s.thLm = o; o += sizeof(double) * (calib ? (size_t)BW * 24 : 0);
   s.zm = o; o += sizeof(double) * ((size_t)6 * BW + 4);
-  s.dinv = o; o += sizeof(double) * 2 * 36;
-  s.pbuf = o; o += sizeof(double) * (size_t)(BW + 1) * 36;
+  s.linv = o; o += sizeof(double) * 2 * 36;
+  s.pbuf = o; o += sizeof(double) * (size_t)(BW + 1) * kWB;
   s.cbuf = o; o += sizeof(double) * 2 * 36;
-  s.tbuf = o; o += sizeof(double) * 24;
+  s.tbuf = o; o += sizeof(double) * 48;
   s.pairs = o; o += sizeof(short2) * (size_t)(BW * (BW + 1) / 2 + 1);
   o = (o + 7) & ~size_t(7);
   s.xo = o; o += sizeof(double) * ((size_t)6 * nb + 4);  // refinement: the unrefined step
@@ -133,79 +137,62 @@ __host__ __device__ inline SolveSmem solve_smem_layout(int nb, int BW, int calib
   return s;
 }
 
-// inverse of a symmetric 3x3 (row-major m) via the adjugate; leading minors check SPD
-__device__ __forceinline__ bool inv3_spd(const double m[9], double o[9]) {
-  const double c00 = m[4] * m[8] - m[5] * m[7];
-  const double c01 = m[5] * m[6] - m[3] * m[8];
-  const double c02 = m[3] * m[7] - m[4] * m[6];
-  const double det = m[0] * c00 + m[1] * c01 + m[2] * c02;
-  const double m2 = m[0] * m[4] - m[1] * m[3];
-  const bool ok = (m[0] > 0.0) && (m2 > 0.0) && (det > 0.0) && isfinite(det);
-  const double id = 1.0 / (ok ? det : 1.0);
-  o[0] = c00 * id;
-  o[1] = (m[2] * m[7] - m[1] * m[8]) * id;
-  o[2] = (m[1] * m[5] - m[2] * m[4]) * id;
-  o[3] = c01 * id;
-  o[4] = (m[0] * m[8] - m[2] * m[6]) * id;
-  o[5] = (m[2] * m[3] - m[0] * m[5]) * id;
-  o[6] = c02 * id;
-  o[7] = (m[1] * m[6] - m[0] * m[7]) * id;
-  o[8] = (m[0] * m[4] - m[1] * m[3]) * id;
+// 1/sqrt(v) to ~1 ulp: the MUFU estimate and two Newton steps (no IEEE sqrt / division
+// sequence on the pivot chain)
+__device__ __forceinline__ double rsqrt64(double v) {
+  double r;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(v));
+  const double h = 0.5 * v;
+  r = r * fma(-h * r, r, 1.5);
+  return r * fma(-h * r, r, 1.5);
+}
+
+// Cholesky factor C of a 6x6 SPD block (+ lam I; the block is symmetrised; right-looking,
+// so each column's trailing updates are independent), returned as Li = C^-1 (lower
+// triangular, row-major, zeros above the diagonal).  false when a pivot is not positive
+// (the block is not SPD).
+__device__ __forceinline__ bool chol6_inv(const double* D, double lam, double* Li) {
+  double a[6][6], ri[6];
+  bool ok = true;
+#pragma unroll
+  for (int i = 0; i < 6; ++i)
+#pragma unroll
+    for (int j = 0; j <= i; ++j) a[i][j] = 0.5 * (D[6 * i + j] + D[6 * j + i]) + (i == j ? lam : 0.0);
+#pragma unroll
+  for (int j = 0; j < 6; ++j) {
+    const double v0 = a[j][j];
+    ok = ok && v0 > 0.0 && isfinite(v0);
+    const double v = ok ? v0 : 1.0;
+    const double r = rsqrt64(v);
+    ri[j] = r;
+    a[j][j] = v * r;
+#pragma unroll
+    for (int i = j + 1; i < 6; ++i) a[i][j] *= r;
+#pragma unroll
+    for (int i = j + 1; i < 6; ++i)
+#pragma unroll
+      for (int k = j + 1; k <= i; ++k) a[i][k] = fma(-a[i][j], a[k][j], a[i][k]);
+  }
+#pragma unroll
+  for (int i = 0; i < 6; ++i) {
+#pragma unroll
+    for (int j = 0; j < 6; ++j) {
+      double v = 0.0;
+      if (j < i) {
+#pragma unroll
+        for (int k = j; k < i; ++k) v = fma(a[i][k], Li[6 * k + j], v);
+        v = -v * ri[i];
+      } else if (j == i) {
+        v = ri[i];
+      }
+      Li[6 * i + j] = v;
+    }
+  }
   return ok;
 }
 
-// inverse of a 6x6 SPD block (+ lam I) via [A B; B^T C]:  A^-1, T = A^-1 B,
-// C' = C - B^T T, D^-1 = [A^-1 + T C'^-1 T^T, -T C'^-1; -C'^-1 T^T, C'^-1].
-__device__ __forceinline__ bool inv6_spd(const double* D, double lam, double* Di) {
-  double A[9], B[9], C[9], Ai[9], T[9], Cs[9], Ci[9], U[9];
-#pragma unroll
-  for (int r = 0; r < 3; ++r)
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      A[3 * r + c] = 0.5 * (D[6 * r + c] + D[6 * c + r]) + (r == c ? lam : 0.0);
-      B[3 * r + c] = D[6 * r + c + 3];
-      C[3 * r + c] = 0.5 * (D[6 * (r + 3) + c + 3] + D[6 * (c + 3) + r + 3]) + (r == c ? lam : 0.0);
-    }
-  bool ok = inv3_spd(A, Ai);
-#pragma unroll
-  for (int r = 0; r < 3; ++r)
-#pragma unroll
-    for (int c = 0; c < 3; ++c)
-      T[3 * r + c] = Ai[3 * r] * B[c] + Ai[3 * r + 1] * B[3 + c] + Ai[3 * r + 2] * B[6 + c];
-#pragma unroll
-  for (int r = 0; r < 3; ++r)
-#pragma unroll
-    for (int c = 0; c < 3; ++c)
-      Cs[3 * r + c] = C[3 * r + c] - (B[r] * T[c] + B[3 + r] * T[3 + c] + B[6 + r] * T[6 + c]);
-#pragma unroll
-  for (int r = 0; r < 3; ++r)
-#pragma unroll
-    for (int c = r + 1; c < 3; ++c) {
-      const double v = 0.5 * (Cs[3 * r + c] + Cs[3 * c + r]);
-      Cs[3 * r + c] = v;
-      Cs[3 * c + r] = v;
-    }
-  ok = inv3_spd(Cs, Ci) && ok;
-#pragma unroll
-  for (int r = 0; r < 3; ++r)
-#pragma unroll
-    for (int c = 0; c < 3; ++c)
-      U[3 * r + c] = T[3 * r] * Ci[c] + T[3 * r + 1] * Ci[3 + c] + T[3 * r + 2] * Ci[6 + c];
-#pragma unroll
-  for (int r = 0; r < 3; ++r)
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      Di[6 * r + c] = Ai[3 * r + c] + U[3 * r] * T[3 * c] + U[3 * r + 1] * T[3 * c + 1] +
-                      U[3 * r + 2] * T[3 * c + 2];
-      Di[6 * r + c + 3] = -U[3 * r + c];
-      Di[6 * (r + 3) + c] = -U[3 * c + r];
-      Di[6 * (r + 3) + c + 3] = Ci[3 * r + c];
-    }
-  return ok;
-}
-
-// 6-vector row times the symmetric D^-1:  out[c] = sum_k v[k] Di[k][c]
-__device__ __forceinline__ void row_times(const double* v, const double* Di, double* out) {
+// W row of a block row v:  out[c] = (v Li^T)[c] = sum_{k <= c} v[k] Li[c][k]
+__device__ __forceinline__ void w_row(const double* v, const double* Li, double* out) {
   double x[6];
 #pragma unroll
   for (int k = 0; k < 6; ++k) x[k] = v[k];
@@ -213,9 +200,27 @@ __device__ __forceinline__ void row_times(const double* v, const double* Di, dou
   for (int c = 0; c < 6; ++c) {
     double s = 0.0;
 #pragma unroll
-    for (int k = 0; k < 6; ++k) s = fma(x[k], Di[6 * k + c], s);
+    for (int k = 0; k <= c; ++k) s = fma(x[k], Li[6 * c + k], s);
     out[c] = s;
   }
+}
+
+// LDL^T factor row from a W row:  out[c] = (w Li)[c] = sum_{k >= c} w[k] Li[k][c]
+__device__ __forceinline__ void l_row(const double* w, const double* Li, double* out) {
+#pragma unroll
+  for (int c = 0; c < 6; ++c) {
+    double s = 0.0;
+#pragma unroll
+    for (int k = c; k < 6; ++k) s = fma(w[k], Li[6 * k + c], s);
+    out[c] = s;
+  }
+}
+
+// entry (r, c) of D^-1 = Li^T Li
+__device__ __forceinline__ double dinv_entry(const double* Li, int r, int c) {
+  double s = 0.0;
+  for (int k = (r > c ? r : c); k < 6; ++k) s = fma(Li[6 * k + r], Li[6 * k + c], s);
+  return s;
 }
 
 // shared-memory working set of one elimination chain
@@ -224,10 +229,10 @@ struct ChainSm {
   double* th;    // theta border: ncols x 24, then theta-theta (16)
   double* thL;   // L_tb per eliminated pivot (ncols x 24)
   double* z;     // rhs: 6 ncols, then theta (4)
-  double* dinv;  // D_b^-1 double buffer
-  double* pbuf;  // panels of the current step
-  double* cbuf;  // critical-warp scratch
-  double* tbuf;  // theta panel
+  double* linv;  // Li_b = C_b^-1 double buffer
+  double* pbuf;  // W panels of the current step (blocks kWB apart)
+  double* cbuf;  // critical-warp scratch: W_{b+1,b} rows [0, 36), y_b = Li_b z_b at 48 + 6 (b & 1)
+  double* tbuf;  // theta panel: W_tb [0, 24), L_tb [24, 48)
   short2* pairs;
   double* ring;
   unsigned long long* bars;
@@ -269,10 +274,16 @@ __device__ inline void chain_forward(const ChainSm& S, const double* band, doubl
     for (int ao = 0; ao < BW; ++ao)
       for (int pi = 0; pi <= ao; ++pi) S.pairs[q++] = make_short2((short)ao, (short)pi);
   }
+  double* const ybuf = S.cbuf + 48;  // y_b = Li_b z_b, double-buffered
   if (npiv > 0 && crit && lane == 0) {
-    double Di[36];
-    if (!inv6_spd(S.win + (size_t)BW * kWB, lam, Di)) *S.fail = 1;  // block (0,0)
-    for (int x = 0; x < 36; ++x) S.dinv[x] = Di[x];
+    double Li[36];
+    if (!chol6_inv(S.win + (size_t)BW * kWB, lam, Li)) *S.fail = 1;  // block (0,0)
+    for (int x = 0; x < 36; ++x) S.linv[x] = Li[x];
+    for (int r = 0; r < 6; ++r) {
+      double v = 0.0;
+      for (int k = 0; k <= r; ++k) v = fma(Li[6 * r + k], S.z[k], v);
+      ybuf[r] = v;
+    }
   }
   __syncthreads();
 #ifdef DBA_CRIT_PROF
@@ -287,38 +298,39 @@ __device__ inline void chain_forward(const ChainSm& S, const double* band, doubl
 #endif
     const int amax = min(nrows - 1, b + BW);
     const int na = amax - b;
-    const double* Db = S.dinv + 36 * (b & 1);  // D_b^-1
+    const double* Lib = S.linv + 36 * (b & 1);  // Li_b
+    const double* yb = ybuf + 6 * (b & 1);      // y_b
     auto wb = [&](int a, int c) -> double* {
       int sl = sb + (a - b);
       sl = sl >= W1 ? sl - W1 : sl;
       return S.win + ((size_t)sl * W1 + (c - a + BW)) * kWB;
     };
-    const double* zb = S.z + 6 * b;
     if (crit) {
-      // next pivot: L_{b+1,b} = S_{b+1,b} D_b^-1, S_{b+1,b+1} -= L S^T, D_{b+1}^-1
+      // next pivot: W_{b+1,b} = S_{b+1,b} Li_b^T, S_{b+1,b+1} -= W W^T, z_{b+1} -= W y_b,
+      // then C_{b+1}, Li_{b+1} and y_{b+1} = Li_{b+1} z_{b+1}
       if (na > 0) {
-        // lane r < 6 owns row r: L_{b+1,b}[r] = S1[r] D_b^-1, then S11[r] -= L[r] S1^T
-        // and z_{b+1}[r] -= L[r] z_b, without exchanging L between lanes (operand
-        // blocks are broadcast loads)
         const double* S1 = wb(b + 1, b);
         double* S11 = wb(b + 1, b + 1);
+        double* Wc = S.cbuf;
+        if (lane < 6) {  // lane r owns row r (the same w_row arithmetic as the panels)
+          double w[6];
+          w_row(S1 + 6 * lane, Lib, w);
+#pragma unroll
+          for (int c = 0; c < 6; ++c) Wc[6 * lane + c] = w[c];
+        }
+        __syncwarp();
         if (lane < 6) {
           const int r = lane;
-          double Lr[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+          double w[6], d[6], zs = S.z[6 * (b + 1) + r];
 #pragma unroll
-          for (int k = 0; k < 6; ++k) {
-            const double sk = S1[6 * r + k];
-#pragma unroll
-            for (int c = 0; c < 6; ++c) Lr[c] = fma(sk, Db[6 * k + c], Lr[c]);
-          }
-          double d[6], zs = S.z[6 * (b + 1) + r];
+          for (int k = 0; k < 6; ++k) w[k] = Wc[6 * r + k];
 #pragma unroll
           for (int c = 0; c < 6; ++c) d[c] = S11[6 * r + c];
 #pragma unroll
           for (int k = 0; k < 6; ++k) {
 #pragma unroll
-            for (int c = 0; c < 6; ++c) d[c] = fma(-Lr[k], S1[6 * c + k], d[c]);
-            zs = fma(-Lr[k], zb[k], zs);
+            for (int c = 0; c < 6; ++c) d[c] = fma(-w[k], Wc[6 * c + k], d[c]);
+            zs = fma(-w[k], yb[k], zs);
           }
 #pragma unroll
           for (int c = 0; c < 6; ++c) S11[6 * r + c] = d[c];  // non-pivot rows are exported from here
@@ -327,12 +339,23 @@ __device__ inline void chain_forward(const ChainSm& S, const double* band, doubl
         CRIT_MARK(0);
         __syncwarp();
         CRIT_MARK(1);
-        if (lane == 0 && b + 1 < npiv) {
-          double Di[36];
-          if (!inv6_spd(S11, lam, Di)) *S.fail = 1;
-          double* Dnx = S.dinv + 36 * ((b + 1) & 1);
+        if (b + 1 < npiv) {
+          double* Lnx = S.linv + 36 * ((b + 1) & 1);
+          if (lane == 0) {  // C_{b+1}, Li_{b+1}, y_{b+1} = Li_{b+1} z_{b+1} from registers
+            double Li[36], zn[6];
+            if (!chol6_inv(S11, lam, Li)) *S.fail = 1;
 #pragma unroll
-          for (int x = 0; x < 36; ++x) Dnx[x] = Di[x];
+            for (int k = 0; k < 6; ++k) zn[k] = S.z[6 * (b + 1) + k];
+#pragma unroll
+            for (int r = 0; r < 6; ++r) {
+              double v = 0.0;
+#pragma unroll
+              for (int k = 0; k <= r; ++k) v = fma(Li[6 * r + k], zn[k], v);
+              ybuf[6 * ((b + 1) & 1) + r] = v;
+            }
+#pragma unroll
+            for (int x = 0; x < 36; ++x) Lnx[x] = Li[x];
+          }
         }
         __syncwarp();
         CRIT_MARK(2);
@@ -351,26 +374,36 @@ __device__ inline void chain_forward(const ChainSm& S, const double* band, doubl
         }
         asm volatile("cp.async.commit_group;");
       }
-      // D_b^-1 -> the diagonal slot of factor row b (threads past the panel rows)
-      if (gt >= kTrailThreads - 64 && gt < kTrailThreads - 28)
-        Lband[((size_t)b * W1 + BW) * 36 + (gt - (kTrailThreads - 64))] = Db[gt - (kTrailThreads - 64)];
-      // panels L_ab = S_ab D_b^-1 (a in (b, amax]), L_tb = S_tb D_b^-1
+      // D_b^-1 = Li_b^T Li_b -> the diagonal slot of factor row b (threads past the panel rows)
+      if (gt >= kTrailThreads - 64 && gt < kTrailThreads - 28) {
+        const int e = gt - (kTrailThreads - 64);
+        Lband[((size_t)b * W1 + BW) * 36 + e] = dinv_entry(Lib, e / 6, e % 6);
+      }
+      // panels W_ab = S_ab Li_b^T (a in (b, amax]) for the updates, L_ab = W_ab Li_b to
+      // the factor rows; W_tb, L_tb of the theta border
       const int prow = 6 * na + (calib ? 4 : 0);
       for (int x = gt; x < prow; x += kTrailThreads) {
+        double w[6], l[6];
         if (x < 6 * na) {
           const int ao = x / 6, r = x % 6;
-          double o[6];
-          row_times(wb(b + 1 + ao, b) + 6 * r, Db, o);
-          double* pb = S.pbuf + 36 * ao + 6 * r;
+          w_row(wb(b + 1 + ao, b) + 6 * r, Lib, w);
+          l_row(w, Lib, l);
+          double* pb = S.pbuf + kWB * ao + 6 * r;
           double* lb = Lband + ((size_t)(b + 1 + ao) * W1 + (BW - 1 - ao)) * 36 + 6 * r;
 #pragma unroll
           for (int c = 0; c < 6; ++c) {
-            pb[c] = o[c];
-            lb[c] = o[c];
+            pb[c] = w[c];
+            lb[c] = l[c];
           }
         } else {
           const int tt = x - 6 * na;
-          row_times(S.th + (size_t)b * 24 + 6 * tt, Db, S.tbuf + 6 * tt);
+          w_row(S.th + (size_t)b * 24 + 6 * tt, Lib, w);
+          l_row(w, Lib, l);
+#pragma unroll
+          for (int c = 0; c < 6; ++c) {
+            S.tbuf[6 * tt + c] = w[c];
+            S.tbuf[24 + 6 * tt + c] = l[c];
+          }
         }
       }
 #ifdef DBA_SOLVE_PROF
@@ -384,7 +417,7 @@ __device__ inline void chain_forward(const ChainSm& S, const double* band, doubl
         g_prof[7] += pb2 - pa;
       }
 #endif
-      // trailing update S_ac -= L_ab S_cb^T (except (b+1,b+1)), border, rhs
+      // trailing update S_ac -= W_ab W_cb^T (except (b+1,b+1)), border, rhs
       const int npair = na * (na + 1) / 2;
       const int n1 = npair * (6 / kTR) * 2;
       const int n2 = calib ? na * 4 : 0;
@@ -401,14 +434,14 @@ __device__ inline void chain_forward(const ChainSm& S, const double* band, doubl
           if (pidx == 0) continue;  // (b+1, b+1): critical warp
           const short2 pr = S.pairs[pidx];
           const int a = b + 1 + pr.x, cc = b + 1 + pr.y;
-          const double* La = S.pbuf + 36 * pr.x + 6 * rr;
-          const double2* Sc = reinterpret_cast<const double2*>(wb(cc, b));
+          const double* Wa = S.pbuf + kWB * pr.x + 6 * rr;
+          const double2* Wc = reinterpret_cast<const double2*>(S.pbuf + kWB * pr.y);
           double* O = wb(a, cc) + 6 * rr + cg;
           double ar[kTR][6], o[kTR][3];
 #pragma unroll
           for (int r = 0; r < kTR; ++r)
 #pragma unroll
-            for (int d = 0; d < 6; ++d) ar[r][d] = La[6 * r + d];
+            for (int d = 0; d < 6; ++d) ar[r][d] = Wa[6 * r + d];
 #pragma unroll
           for (int r = 0; r < kTR; ++r)
 #pragma unroll
@@ -418,7 +451,7 @@ __device__ inline void chain_forward(const ChainSm& S, const double* band, doubl
             double sc[6];
 #pragma unroll
             for (int q = 0; q < 3; ++q) {
-              const double2 v = Sc[3 * (cg + c) + q];
+              const double2 v = Wc[3 * (cg + c) + q];
               sc[2 * q] = v.x;
               sc[2 * q + 1] = v.y;
             }
@@ -434,47 +467,47 @@ __device__ inline void chain_forward(const ChainSm& S, const double* band, doubl
         } else if (x < n1 + n2) {
           const int y2 = x - n1, co = y2 / 4, tt = y2 % 4;
           const int cc = b + 1 + co;
-          const double* Lt = S.tbuf + 6 * tt;
-          const double* Sc = wb(cc, b);
+          const double* Wt = S.tbuf + 6 * tt;
+          const double* Wc = S.pbuf + kWB * co;
           double* O = S.th + (size_t)cc * 24 + 6 * tt;
 #pragma unroll
           for (int c = 0; c < 6; ++c) {
             double s = O[c];
 #pragma unroll
-            for (int d = 0; d < 6; ++d) s = fma(-Lt[d], Sc[6 * c + d], s);
+            for (int d = 0; d < 6; ++d) s = fma(-Wt[d], Wc[6 * c + d], s);
             O[c] = s;
           }
         } else if (x < n1 + n2 + n3) {
           const int tt = x - n1 - n2;
-          const double* Lt = S.tbuf + 6 * tt;
+          const double* Wt = S.tbuf + 6 * tt;
           double* O = S.th + (size_t)ncols * 24 + 4 * tt;
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
-            const double* Su = S.th + (size_t)b * 24 + 6 * u;
+            const double* Wu = S.tbuf + 6 * u;
             double s = O[u];
 #pragma unroll
-            for (int d = 0; d < 6; ++d) s = fma(-Lt[d], Su[d], s);
+            for (int d = 0; d < 6; ++d) s = fma(-Wt[d], Wu[d], s);
             O[u] = s;
           }
         } else {
           const int q = x - n1 - n2 - n3;
-          const double* Lr;
+          const double* Wr;
           double* zt;
           if (q < 6 * (na - 1)) {
-            Lr = S.pbuf + 36 + 6 * q;  // rows a >= b+2
+            Wr = S.pbuf + kWB * (1 + q / 6) + 6 * (q % 6);  // rows a >= b+2
             zt = S.z + 6 * (b + 2) + q;
           } else {
             const int tt = q - 6 * (na > 0 ? na - 1 : 0);
-            Lr = S.tbuf + 6 * tt;
+            Wr = S.tbuf + 6 * tt;
             zt = S.z + 6 * ncols + tt;
           }
           double s = *zt;
 #pragma unroll
-          for (int d = 0; d < 6; ++d) s = fma(-Lr[d], zb[d], s);
+          for (int d = 0; d < 6; ++d) s = fma(-Wr[d], yb[d], s);
           *zt = s;
         }
       }
-      if (calib && gt < 24) S.thL[(size_t)b * 24 + gt] = S.tbuf[gt];  // L_tb for the backward sweep
+      if (calib && gt < 24) S.thL[(size_t)b * 24 + gt] = S.tbuf[24 + gt];  // L_tb for the backward sweep
       if (stage) asm volatile("cp.async.wait_all;" ::: "memory");
     }
 #ifdef DBA_SOLVE_PROF
@@ -698,14 +731,13 @@ __device__ inline void chain_backward(double* z, const double* thL, const double
 }
 
 // ---------------------------------------------------------------- iterative refinement
-// The block LDL^T with explicit 6x6 pivot inverses is backward stable only up to the
-// conditioning of its pivot blocks: on the noisy C3 system (cond(S + lam I) = 6e10) the
-// step is 4e-7 from the exact solution while LAPACK's Cholesky is 9e-9 (measured, an
-// emulation of this algorithm in numpy agrees: scratch/emul_ldl2.py).  One step of
-// iterative refinement with the stored factors -- r = y - (S + lam I) x in float64 from the
-// original band, the same forward / middle / backward substitutions on r, x += c --
-// brings it to 1e-10.  The substitutions reuse the factor rows in global memory and
-// the theta factors still in shared memory.
+// Optional (dba_options.refine).  With the Cholesky-form updates the factorisation is as
+// accurate as LAPACK's (noisy C3 at cond 7e10: 1.1e-8 vs 2.3e-8, the former explicit-inverse
+// LDL^T 1.9e-7; profiles/r02_solve_accuracy.txt).  One step of iterative refinement with
+// the stored factors -- r = y - (S + lam I) x in float64 from the original band, the same
+// forward / middle / backward substitutions on r, x += c -- takes the step to ~1e-10.  The
+// substitutions reuse the factor rows in global memory and the theta factors still in
+// shared memory.
 
 // r[6a + s] of (S + lam I) x = y for pose block a (global order)
 __device__ inline double resid_pose(const SolveArgs& A, const double* x, int a, int s, double lam) {
@@ -804,7 +836,7 @@ __device__ inline ChainSm chain_sm(unsigned char* smem, const SolveSmem& L, int*
   S.th = reinterpret_cast<double*>(smem + (middle ? L.thm : L.th));
   S.thL = reinterpret_cast<double*>(smem + (middle ? L.thLm : L.thL));
   S.z = reinterpret_cast<double*>(smem + (middle ? L.zm : L.z));
-  S.dinv = reinterpret_cast<double*>(smem + L.dinv);
+  S.linv = reinterpret_cast<double*>(smem + L.linv);
   S.pbuf = reinterpret_cast<double*>(smem + L.pbuf);
   S.cbuf = reinterpret_cast<double*>(smem + L.cbuf);
   S.tbuf = reinterpret_cast<double*>(smem + L.tbuf);

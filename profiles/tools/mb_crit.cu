@@ -1,6 +1,6 @@
 // single-warp replica of the critical-warp step (6-lane L/S11 update + lane-0 inv6)
 #include <cstdio>
-#include "../../paper_2411_17660_b200/csrc/dba_solve.cuh"
+#include "old_pivot.cuh"
 using namespace dba;
 template <int MODE>
 __global__ void k(double* out, long long* cyc, int n) {

@@ -1,7 +1,7 @@
 // single-warp replica of a 12x12-pivot critical step: 12 lanes (row each) form
 // L = S1 D^-1 and S11 -= L S1^T, lane 0 inverts the 12x12 block via 2x2 blocks of 6x6
 #include <cstdio>
-#include "../../paper_2411_17660_b200/csrc/dba_solve.cuh"
+#include "old_pivot.cuh"
 using namespace dba;
 __device__ void inv12(const double* S, double* Di) {
   // [A B; B^T C] with 6x6 blocks: Ai = inv6(A); T = Ai B; Cs = C - B^T T; Ci = inv6(Cs)

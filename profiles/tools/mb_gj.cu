@@ -1,7 +1,7 @@
 // crit-step variant: 6 lanes hold the rows of S11' and invert it by Gauss-Jordan with
 // shuffle broadcasts (no lane-0 gather, no serial inverse)
 #include <cstdio>
-#include "../../paper_2411_17660_b200/csrc/dba_solve.cuh"
+#include "old_pivot.cuh"
 using namespace dba;
 __device__ __forceinline__ double rcp_d(double x) { return 1.0 / x; }
 __global__ void k(double* out, long long* cyc, int n, int variant) {

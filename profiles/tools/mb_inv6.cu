@@ -1,6 +1,6 @@
 // isolated latency of inv6_spd (one thread, operands in shared memory)
 #include <cstdio>
-#include "../../paper_2411_17660_b200/csrc/dba_solve.cuh"
+#include "old_pivot.cuh"
 using namespace dba;
 __global__ void k(double* out, long long* cyc, int n) {
   __shared__ double D[36], Di[36];
