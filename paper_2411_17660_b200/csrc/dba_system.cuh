@@ -189,6 +189,7 @@ __global__ void __launch_bounds__(512) assemble_kernel(const AsmArgs A) {
   __shared__ double Th[6 * kMaxOutDegree + 10];
   __shared__ double Tb[kMaxOutDegree * 36];  // per-edge Ad_e^T H_e
   __shared__ double Tc[kMaxOutDegree * 36];  // per-edge pose-block terms
+  __shared__ int t6[36];                      // tri6(r, c) of the packed 6x6 Hessians
   const int fl = blockIdx.x, tid = threadIdx.x;
   const int s0 = A.csr_off[fl], k = A.csr_off[fl + 1] - s0;
   if (k == 0) return;
@@ -198,6 +199,7 @@ __global__ void __launch_bounds__(512) assemble_kernel(const AsmArgs A) {
   double* fv = A.Fbuf + A.off_f[fl];
   const int sg0 = A.frame_seg[fl], sg1 = A.frame_seg[fl + 1];
 
+  if (tid < 36) t6[tid] = tri6(tid / 6, tid % 6);
   // segment partials, summed in segment order; each pass over x issues its loads
   // independently (unrolled) so the loop is bandwidth-, not latency-bound
   for (int x = tid; x < k * 36; x += blockDim.x) Ad[x] = A.adj[36 * (size_t)s0 + x];
@@ -241,7 +243,7 @@ __global__ void __launch_bounds__(512) assemble_kernel(const AsmArgs A) {
     const double* Ae = Ad + 36 * e;
     const double* He = hs + e * nve;
     double hq = 0.0;
-    for (int u = 0; u < 6; ++u) hq += Ae[6 * u + r] * He[tri6(u, q)];
+    for (int u = 0; u < 6; ++u) hq += Ae[6 * u + r] * He[t6[6 * u + q]];
     Tb[x] = hq;
   }
   __syncthreads();
@@ -255,41 +257,49 @@ __global__ void __launch_bounds__(512) assemble_kernel(const AsmArgs A) {
   }
   __syncthreads();
   const int th0 = 6 * k;  // theta offset in u-space
-  for (int x = tid; x < m * m; x += blockDim.x) {
-    const int r = x / m, c = x % m;
-    double v;
-    if (r >= 6 && c >= 6) {
-      const int ru = r - 6, cu = c - 6;
-      double b = 0.0;
-      const bool rt = A.calib && ru >= th0, ct = A.calib && cu >= th0;
-      if (!rt && !ct) {
-        if (ru / 6 == cu / 6) b = hs[(ru / 6) * nve + tri6(ru % 6, cu % 6)];
-      } else if (rt && !ct) {
-        b = hs[(cu / 6) * nve + 32 + 6 * (ru - th0) + cu % 6];
-      } else if (!rt && ct) {
-        b = hs[(ru / 6) * nve + 32 + 6 * (cu - th0) + ru % 6];
+  // F row by row: warp w takes rows w, w + 16, ..., lanes the columns (no per-entry
+  // division by m); packed 6x6 indices from the shared tri6 table
+  const int lane = tid & 31, nwarp = blockDim.x >> 5;
+  for (int r = tid >> 5; r < m; r += nwarp) {
+    const int ru = r - 6;
+    const int rb = ru / 6, rs = ru - 6 * rb;  // (ru >= 0) block and slot of row r in u-space
+    for (int c = lane; c < m; c += 32) {
+      double v;
+      if (r >= 6 && c >= 6) {
+        const int cu = c - 6;
+        const int cb = cu / 6, cs = cu - 6 * cb;
+        double b = 0.0;
+        const bool rt = A.calib && ru >= th0, ct = A.calib && cu >= th0;
+        if (!rt && !ct) {
+          if (rb == cb) b = hs[rb * nve + t6[6 * rs + cs]];
+        } else if (rt && !ct) {
+          b = hs[cb * nve + 32 + 6 * (ru - th0) + cs];
+        } else if (!rt && ct) {
+          b = hs[rb * nve + 32 + 6 * (cu - th0) + rs];
+        } else {
+          b = fs[1 + tri4(ru - th0, cu - th0)];
+        }
+        v = b - Ms[ru * mu + cu];
+      } else if (r < 6 && c < 6) {
+        v = 0.0;
+        for (int e = 0; e < k; ++e) v += Tc[36 * e + 6 * r + c];  // fixed edge order
       } else {
-        b = fs[1 + tri4(ru - th0, cu - th0)];
+        const int rr = r < 6 ? r : c;          // pose-i row (0..5)
+        const int cu = r < 6 ? c - 6 : r - 6;  // u-space column
+        double b = 0.0;
+        if (A.calib && cu >= th0) {
+          const int t = cu - th0;
+          for (int e = 0; e < k; ++e)
+            for (int q = 0; q < 6; ++q) b -= hs[e * nve + 32 + 6 * t + q] * Ad[36 * e + 6 * q + rr];
+        } else {
+          const int e = cu / 6, cc = cu - 6 * e;
+#pragma unroll
+          for (int q = 0; q < 6; ++q) b -= Ad[36 * e + 6 * q + rr] * hs[e * nve + t6[6 * q + cc]];
+        }
+        v = b + Nm[rr * mu + cu];  // B_iu - (T M T^T)_iu with T_i = -Ad^T
       }
-      v = b - Ms[ru * mu + cu];
-    } else if (r < 6 && c < 6) {
-      v = 0.0;
-      for (int e = 0; e < k; ++e) v += Tc[36 * e + 6 * r + c];  // fixed edge order
-    } else {
-      const int rr = r < 6 ? r : c;          // pose-i row (0..5)
-      const int cu = r < 6 ? c - 6 : r - 6;  // u-space column
-      double b = 0.0;
-      if (A.calib && cu >= th0) {
-        const int t = cu - th0;
-        for (int e = 0; e < k; ++e)
-          for (int q = 0; q < 6; ++q) b -= hs[e * nve + 32 + 6 * t + q] * Ad[36 * e + 6 * q + rr];
-      } else {
-        const int e = cu / 6, cc = cu % 6;
-        for (int q = 0; q < 6; ++q) b -= Ad[36 * e + 6 * q + rr] * hs[e * nve + tri6(q, cc)];
-      }
-      v = b + Nm[rr * mu + cu];  // B_iu - (T M T^T)_iu with T_i = -Ad^T
+      F[r * m + c] = v;
     }
-    F[x] = v;
   }
   for (int x = tid; x < m; x += blockDim.x) {
     double v;
