@@ -250,22 +250,37 @@ def test_damping_candidates_bitwise(torch_cuda, name, kf, calib):
         assert list(r.energy_trace) == list(r1.energy_trace)
 
 
-def test_loop_graph_matches_stream_path(torch_cuda, monkeypatch):
-    """DBA_GRAPH=1 runs dba_solve's LM loop as one CUDA graph (WHILE over rounds, IF
-    nodes for later damping candidates and the linearisation); it must reproduce the
-    stream path bit for bit, rejections included."""
+@pytest.mark.parametrize("cfg", ["C3", "C4", "C5"])
+def test_loop_graph_matches_stream_path(torch_cuda, monkeypatch, cfg):
+    """The LM loop as one CUDA graph (WHILE over rounds, IF nodes for later damping
+    candidates and the linearisation) must reproduce the stream path bit for bit,
+    rejections included, with a prior (C4) and with intrinsics (C5): forced on
+    (DBA_GRAPH=1, the second run reusing the instantiated graph) and in the default auto
+    mode (a call repeating the previous call's buffers and options runs the graph)."""
     from paper_2411_17660_b200 import dba, scenes
-    wl = scenes.make_workload("C3", height=24, width=32, keyframes=64)
-    s = dba.DBASolver(wl.ii, wl.jj, len(wl.frames), 24, 32, wl.fixed)
+    kf = {"C3": 64, "C4": 25, "C5": 32}[cfg]
+    wl = scenes.make_workload(cfg, height=24, width=32, keyframes=kf, noise=0.5 if cfg != "C3" else 0.0)
+    calib, prior = cfg == "C5", cfg == "C4"
+    s = dba.DBASolver(wl.ii, wl.jj, len(wl.frames), 24, 32, wl.fixed, optimize_intrinsics=calib,
+                      use_prior=prior)
+    torch = torch_cuda
+    dev = torch.device("cuda")
+    args = [torch.as_tensor(x, device=dev) for x in (wl.poses0, wl.disps0, wl.intr0, wl.flow)]
+    kw = {k: torch.as_tensor(v, device=dev) for k, v in (dict(prior=wl.prior, prior_mask=wl.prior_mask)
+                                                         if prior else {}).items()}
     outs = []
-    for g in ("0", "1", "1"):  # the second graph run reuses the instantiated graph
-        monkeypatch.setenv("DBA_GRAPH", g)
-        Po, Do, Ko, rep = s.solve(wl.poses0, wl.disps0, wl.intr0, wl.flow, iters=12)
-        outs.append((Po.cpu().numpy(), Do.cpu().numpy(), rep))
-    P0, D0, r0 = outs[0]
-    assert r0.trials > r0.iterations_run  # rejections exercised
-    for P, D, r in outs[1:]:
-        assert np.array_equal(P, P0) and np.array_equal(D, D0)
+    for g in ("0", "1", "1", None, None, None):
+        if g is None:
+            monkeypatch.delenv("DBA_GRAPH", raising=False)
+        else:
+            monkeypatch.setenv("DBA_GRAPH", g)
+        Po, Do, Ko, rep = s.solve(*args, iters=12, **kw)
+        outs.append((Po.cpu().numpy(), Do.cpu().numpy(), Ko.cpu().numpy(), rep))
+    P0, D0, K0, r0 = outs[0]
+    if cfg == "C3":
+        assert r0.trials > r0.iterations_run  # rejections exercised
+    for P, D, K, r in outs[1:]:
+        assert np.array_equal(P, P0) and np.array_equal(D, D0) and np.array_equal(K, K0)
         assert (r.trials, r.iterations_run, r.final_energy) == (r0.trials, r0.iterations_run, r0.final_energy)
 
 
