@@ -388,6 +388,35 @@ __global__ void gather_kernel(const GatherArgs A) {
   if (wid >= A.n_units) return;
   const GatherUnit u = A.units[wid];
   const int n = u.rows * u.cols;
+  if (n <= 64) {
+    // every unit of the band (6x6, 4x6, 4x4 blocks, rhs rows): a lane owns elements lane and
+    // lane + 32; the contribution list is read coalesced, 32 at a time, and broadcast by
+    // shuffles, so the Fbuf loads of successive contributions are independent (the sum
+    // order per element is the list order, as before)
+    const int e0 = lane, e1 = lane + 32;
+    const int r0 = e0 / u.cols, k0 = e0 - r0 * u.cols, r1 = e1 / u.cols, k1 = e1 - r1 * u.cols;
+    double s0 = 0.0, s1 = 0.0;
+    for (int q0 = u.c0; q0 < u.c1; q0 += 32) {
+      const int nq = min(32, u.c1 - q0);
+      long long src = 0;
+      int stride = 0;
+      if (lane < nq) {
+        const Contrib cb = A.contrib[q0 + lane];
+        src = cb.src;
+        stride = cb.stride;
+      }
+#pragma unroll 4
+      for (int j = 0; j < nq; ++j) {
+        const long long sj = __shfl_sync(0xffffffffu, src, j);
+        const long long tj = __shfl_sync(0xffffffffu, stride, j);
+        if (e0 < n) s0 += A.Fbuf[sj + (u.trans ? k0 * tj + r0 : r0 * tj + k0)];
+        if (e1 < n) s1 += A.Fbuf[sj + (u.trans ? k1 * tj + r1 : r1 * tj + k1)];
+      }
+    }
+    if (e0 < n) A.sys[u.dst + e0] = s0;
+    if (e1 < n) A.sys[u.dst + e1] = s1;
+    return;
+  }
   for (int e = lane; e < n; e += 32) {
     const int r = e / u.cols, c = e % u.cols;
     double s = 0.0;
