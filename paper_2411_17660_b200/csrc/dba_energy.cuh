@@ -62,6 +62,7 @@ __global__ void __launch_bounds__(kEnergyThreads, 4) energy_kernel(const EnergyA
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ double red[kEnergyThreads / 32];
   __shared__ double kappa_s;
+  __shared__ double rcp_s[8];  // 1/fx_c, 1/fy_c, 1/fx_n, 1/fy_n, fx_c/fy_c, fy_c/fx_c (one thread)
   const int fl = blockIdx.x / A.tiles, tile = blockIdx.x % A.tiles;
   const int s0 = A.csr_off[fl], k = A.csr_off[fl + 1] - s0;
   const int f = A.frame_of[fl];
@@ -78,6 +79,14 @@ __global__ void __launch_bounds__(kEnergyThreads, 4) energy_kernel(const EnergyA
     for (int x = tid; x < k * (int)(sizeof(EdgeBack) / 8); x += kEnergyThreads)
       reinterpret_cast<double*>(sb)[x] = reinterpret_cast<const double*>(A.back + s0)[x];
   for (int x = tid; x < k; x += kEnergyThreads) fp0[x] = A.flow + (size_t)A.slot_flow[s0 + x] * P;
+  if (tid == 0) {
+    rcp_s[0] = 1.0 / A.intr_c[0];
+    rcp_s[1] = 1.0 / A.intr_c[1];
+    rcp_s[2] = 1.0 / A.intr_n[0];
+    rcp_s[3] = 1.0 / A.intr_n[1];
+    rcp_s[4] = A.intr_c[0] * rcp_s[1];
+    rcp_s[5] = A.intr_c[1] * rcp_s[0];
+  }
   __syncthreads();
   const double dth[4] = {A.intr_n[0] - A.intr_c[0], A.intr_n[1] - A.intr_c[1], A.intr_n[2] - A.intr_c[2],
                          A.intr_n[3] - A.intr_c[3]};
@@ -114,7 +123,7 @@ __global__ void __launch_bounds__(kEnergyThreads, 4) energy_kernel(const EnergyA
   asm volatile("cp.async.wait_all;" ::: "memory");
   if (phaseA) {
     const double fxc = A.intr_c[0], fyc = A.intr_c[1], cxc = A.intr_c[2], cyc = A.intr_c[3];
-    const double qx = (pu - cxc) / fxc, qy = (pv - cyc) / fyc;
+    const double qx = (pu - cxc) * rcp_s[0], qy = (pv - cyc) * rcp_s[1];
     double Cp = 0.0, gdp = 0.0, accp = 0.0;
     for (int a = 0; a < k; ++a) {
       const EdgeBack& e = sb[a];
@@ -130,7 +139,7 @@ __global__ void __launch_bounds__(kEnergyThreads, 4) energy_kernel(const EnergyA
                   fyc * (-(1.0 + T.yt * T.yt) * dl[3] + T.xt * T.yt * dl[4] + T.xt * dl[5]);
       if (CALIB) {
         double Tu[4], Tv[4];
-        theta_jac(e.R, T, qx, qy, fxc, fyc, Tu, Tv);
+        theta_jac(e.R, T, qx, qy, rcp_s[4], rcp_s[5], Tu, Tv);
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
           ju += Tu[r] * dth[r];
@@ -153,7 +162,7 @@ __global__ void __launch_bounds__(kEnergyThreads, 4) energy_kernel(const EnergyA
   }
   // residual energy at (x_n, d_n)
   if (in) A.d_new[fpx] = dn;
-  const double qx = (pu - cxn) / fxn, qy = (pv - cyn) / fyn;
+  const double qx = (pu - cxn) * rcp_s[2], qy = (pv - cyn) * rcp_s[3];
   double ed = 0.0;
   for (int a = 0; a < k; ++a) {
     const EdgeLin& e = sl[a];

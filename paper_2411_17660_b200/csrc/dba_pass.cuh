@@ -246,18 +246,20 @@ __device__ __forceinline__ PixTerms pix_terms(const double R[9], const double t[
   return o;
 }
 
-// J_theta = d(u,v)/d(fx,fy,cx,cy) through unprojection and projection
-__device__ __forceinline__ void theta_jac(const double R[9], const PixTerms& T, double qx, double qy, double fx,
-                                          double fy, double Tu[4], double Tv[4]) {
+// J_theta = d(u,v)/d(fx,fy,cx,cy) through unprojection and projection; fxy = fx / fy and
+// fyx = fy / fx are formed once per thread by the caller (four divisions per edge-pixel
+// otherwise)
+__device__ __forceinline__ void theta_jac(const double R[9], const PixTerms& T, double qx, double qy, double fxy,
+                                          double fyx, double Tu[4], double Tv[4]) {
   const double cu0 = T.iz * (R[0] - T.xt * R[6]), cu1 = T.iz * (R[1] - T.xt * R[7]);
   const double cv0 = T.iz * (R[3] - T.yt * R[6]), cv1 = T.iz * (R[4] - T.yt * R[7]);
   Tu[0] = T.xt - cu0 * qx;
-  Tu[1] = -cu1 * qy * fx / fy;
+  Tu[1] = -cu1 * qy * fxy;
   Tu[2] = 1.0 - cu0;
-  Tu[3] = -cu1 * fx / fy;
-  Tv[0] = -cv0 * qx * fy / fx;
+  Tu[3] = -cu1 * fxy;
+  Tv[0] = -cv0 * qx * fyx;
   Tv[1] = T.yt - cv1 * qy;
-  Tv[2] = -cv0 * fy / fx;
+  Tv[2] = -cv0 * fyx;
   Tv[3] = 1.0 - cv1;
 }
 
@@ -540,6 +542,9 @@ __global__ void __launch_bounds__(kPassCTA, 1) pass_kernel(const PassArgs A) {
   const double Wf = (double)A.W, Hf = (double)A.H;
   const double fxn = A.intr_n[0], fyn = A.intr_n[1], cxn = A.intr_n[2], cyn = A.intr_n[3];
   const double fxc = A.intr_c[0], fyc = A.intr_c[1], cxc = A.intr_c[2], cyc = A.intr_c[3];
+  // reciprocals and ratios of the intrinsics, once per thread (per-pixel rays, J_theta)
+  const double ifxn = 1.0 / fxn, ifyn = 1.0 / fyn, ifxc = 1.0 / fxc, ifyc = 1.0 / fyc;
+  const double fxyn = fxn * ifyn, fyxn = fyn * ifxn, fxyc = fxc * ifyc, fyxc = fyc * ifxc;
   const double dth[4] = {fxn - fxc, fyn - fyc, cxn - cxc, cyn - cyc};
   int tau = 0;
 
@@ -630,8 +635,8 @@ __global__ void __launch_bounds__(kPassCTA, 1) pass_kernel(const PassArgs A) {
       for (int x = tid; x < SUB; x += kPassThreads) {
         const int p = pbase + x;
         const double pu = (double)(p % A.W), pv = (double)(p / A.W);
-        qcs[x] = make_double2((pu - cxc) / fxc, (pv - cyc) / fyc);
-        qns[x] = make_double2((pu - cxn) / fxn, (pv - cyn) / fyn);
+        qcs[x] = make_double2((pu - cxc) * ifxc, (pv - cyc) * ifyc);
+        qns[x] = make_double2((pu - cxn) * ifxn, (pv - cyn) * ifyn);
       }
       nbar_sync(kBarGeo, kPassThreads);
       // the next tile's records land in the other buffer under this tile's work (its last
@@ -661,7 +666,7 @@ __global__ void __launch_bounds__(kPassCTA, 1) pass_kernel(const PassArgs A) {
                         fyc * (-(1.0 + T.yt * T.yt) * dl[3] + T.xt * T.yt * dl[4] + T.xt * dl[5]);
             if (CALIB) {
               double Tu[4], Tv[4];
-              theta_jac(e.R, T, qx, qy, fxc, fyc, Tu, Tv);
+              theta_jac(e.R, T, qx, qy, fxyc, fyxc, Tu, Tv);
 #pragma unroll
               for (int r = 0; r < 4; ++r) {
                 ju += Tu[r] * dth[r];
@@ -772,7 +777,7 @@ __global__ void __launch_bounds__(kPassCTA, 1) pass_kernel(const PassArgs A) {
         }
         if (CALIB) {
           double Tu[4], Tv[4];
-          theta_jac(e.R, T, qx, qy, fxn, fyn, Tu, Tv);
+          theta_jac(e.R, T, qx, qy, fxyn, fyxn, Tu, Tv);
           double v32[32];
 #pragma unroll
           for (int r = 0; r < 4; ++r)
