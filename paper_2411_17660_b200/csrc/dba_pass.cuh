@@ -825,7 +825,7 @@ __global__ void __launch_bounds__(kPassCTA, 1) pass_kernel(const PassArgs A) {
           facc[0] += ap * dd * dd;
           fpri = fma(dn * ap, dd, fpri);
         }
-        icv[pl] = (in && !A.freeze) ? __drcp_rn(C) : 0.0;  // frozen d: no fill-in
+        icv[pl] = (in && !A.freeze) ? rcp64(C) : 0.0;  // frozen d: no fill-in
         if (CALIB) {
           double Et[4] = {0.0, 0.0, 0.0, 0.0};
           for (int a = 0; a < k; ++a)
@@ -836,7 +836,7 @@ __global__ void __launch_bounds__(kPassCTA, 1) pass_kernel(const PassArgs A) {
         }
         // second extra column: A5 gauge c = C/d, or (scalefix) c = d (eta + alpha m), whose
         // E C^-1 c is the reduced system's exact row along the monocular scale direction
-        const double cx = A.scalefix ? dn * (A.eta + ap) : C / dn;
+        const double cx = A.scalefix ? dn * (A.eta + ap) : C * rcp64(dn);
         U[mu * US + pl] = gd;
         U[(mu + 1) * US + pl] = in ? cx : 0.0;
       }
