@@ -62,7 +62,7 @@ __global__ void __launch_bounds__(kEnergyThreads, 4) energy_kernel(const EnergyA
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ double red[kEnergyThreads / 32];
   __shared__ double kappa_s;
-  __shared__ double rcp_s[8];  // 1/fx_c, 1/fy_c, 1/fx_n, 1/fy_n, fx_c/fy_c, fy_c/fx_c (one thread)
+  __shared__ double rcp_s[8];  // 1/fx_c, 1/fy_c, 1/fx_n, 1/fy_n, fx_c/fy_c, fy_c/fx_c, 1/W (one thread)
   const int fl = blockIdx.x / A.tiles, tile = blockIdx.x % A.tiles;
   const int s0 = A.csr_off[fl], k = A.csr_off[fl + 1] - s0;
   const int f = A.frame_of[fl];
@@ -86,6 +86,7 @@ __global__ void __launch_bounds__(kEnergyThreads, 4) energy_kernel(const EnergyA
     rcp_s[3] = 1.0 / A.intr_n[1];
     rcp_s[4] = A.intr_c[0] * rcp_s[1];
     rcp_s[5] = A.intr_c[1] * rcp_s[0];
+    rcp_s[6] = 1.0 / (double)A.W;
   }
   __syncthreads();
   const double dth[4] = {A.intr_n[0] - A.intr_c[0], A.intr_n[1] - A.intr_c[1], A.intr_n[2] - A.intr_c[2],
@@ -114,7 +115,8 @@ __global__ void __launch_bounds__(kEnergyThreads, 4) energy_kernel(const EnergyA
   asm volatile("cp.async.commit_group;");
   const double Wf = (double)A.W, Hf = (double)A.H;
   const double fxn = A.intr_n[0], fyn = A.intr_n[1], cxn = A.intr_n[2], cyn = A.intr_n[3];
-  const double pu = (double)(pc % A.W), pv = (double)(pc / A.W);
+  const double pd = (double)pc;
+  const double pv = floor((pd + 0.5) * rcp_s[6]), pu = fma(-pv, Wf, pd);  // exact: p < 2^40
   const size_t fpx = (size_t)f * P + pc;
   const double dc = A.d_cur[fpx];
   double dn = dc;

@@ -545,6 +545,7 @@ __global__ void __launch_bounds__(kPassCTA, 1) pass_kernel(const PassArgs A) {
   // reciprocals and ratios of the intrinsics, once per thread (per-pixel rays, J_theta)
   const double ifxn = 1.0 / fxn, ifyn = 1.0 / fyn, ifxc = 1.0 / fxc, ifyc = 1.0 / fyc;
   const double fxyn = fxn * ifyn, fyxn = fyn * ifxn, fxyc = fxc * ifyc, fyxc = fyc * ifxc;
+  const double iW = 1.0 / Wf;  // pixel index -> (u, v) without integer division
   const double dth[4] = {fxn - fxc, fyn - fyc, cxn - cxc, cyn - cyc};
   int tau = 0;
 
@@ -633,8 +634,8 @@ __global__ void __launch_bounds__(kPassCTA, 1) pass_kernel(const PassArgs A) {
       const double* const dcs = dcsb + (tau & 1) * SUB;
       asm volatile("cp.async.wait_all;" ::: "memory");
       for (int x = tid; x < SUB; x += kPassThreads) {
-        const int p = pbase + x;
-        const double pu = (double)(p % A.W), pv = (double)(p / A.W);
+        const double pd = (double)(pbase + x);
+        const double pv = floor((pd + 0.5) * iW), pu = fma(-pv, Wf, pd);  // exact: p < 2^40
         qcs[x] = make_double2((pu - cxc) * ifxc, (pv - cyc) * ifyc);
         qns[x] = make_double2((pu - cxn) * ifxn, (pv - cyn) * ifyn);
       }
