@@ -63,7 +63,7 @@ __global__ void __launch_bounds__(kEnergyThreads, 4) energy_kernel(const EnergyA
   __shared__ double red[kEnergyThreads / 32];
   __shared__ double kappa_s;
   __shared__ double rcp_s[8];  // 1/fx_c, 1/fy_c, 1/fx_n, 1/fy_n, fx_c/fy_c, fy_c/fx_c, 1/W (one thread)
-  const int fl = blockIdx.x / A.tiles, tile = blockIdx.x % A.tiles;
+  const int fl = blockIdx.y, tile = blockIdx.x;  // grid (tiles, frames)
   const int s0 = A.csr_off[fl], k = A.csr_off[fl + 1] - s0;
   const int f = A.frame_of[fl];
   float4* fs = reinterpret_cast<float4*>(smem);  // [kmax][256]
@@ -185,7 +185,7 @@ __global__ void __launch_bounds__(kEnergyThreads, 4) energy_kernel(const EnergyA
     double s = 0.0;
 #pragma unroll
     for (int w = 0; w < kEnergyThreads / 32; ++w) s += red[w];
-    A.part[blockIdx.x] = s;
+    A.part[blockIdx.y * A.tiles + blockIdx.x] = s;
   }
 }
 

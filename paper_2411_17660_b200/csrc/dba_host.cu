@@ -1198,7 +1198,7 @@ int launch_epass(Ctx& c, int cur, int nxt, bool backsub, int cand = 0) {
     if (int s = ev_pair(c, ev)) return s;
     DBA_CUDA(cudaEventRecord(pr.pool[ev.first], c.st));
   }
-  if (int s = launch(c, k, dim3(p->NL * a.tiles), dim3(kEnergyThreads), smem, false, a)) return s;
+  if (int s = launch(c, k, dim3(a.tiles, p->NL), dim3(kEnergyThreads), smem, false, a)) return s;
   mark(c, "pass-E");
   pr.energy_launches++;
   if (pr.on) {
