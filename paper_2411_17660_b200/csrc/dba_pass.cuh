@@ -409,7 +409,7 @@ __global__ void __launch_bounds__(kPassCTA, 1) pass_kernel(const PassArgs A) {
     // ============================================================== product warps
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(pass_gemm_regs(QMAX)));
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    int tau = 0;
+    int tau = 0, slot = 0;  // tile sequence number and its ring slot (tau mod NS)
     for (int sg = sg0; sg < sg1; ++sg) {
       const int fl = A.seg_frame[sg];
       const int k = A.csr_off[fl + 1] - A.csr_off[fl];
@@ -479,8 +479,8 @@ __global__ void __launch_bounds__(kPassCTA, 1) pass_kernel(const PassArgs A) {
           }
         }
       };
-      for (int tile = A.seg_t0[sg]; tile < A.seg_t1[sg]; ++tile, ++tau) {
-        const int b = tau % NS;
+      for (int tile = A.seg_t0[sg]; tile < A.seg_t1[sg]; ++tile, ++tau, slot = slot + 1 == NS ? 0 : slot + 1) {
+        const int b = slot;
         nbar_sync(kBarFull + b, kPassCTA);
         gemm(Ubuf + b * ulen, icvb + b * SUB);
         if (tau + NS < ntot) nbar_arrive(kBarEmpty + b, kPassCTA);
@@ -547,7 +547,7 @@ __global__ void __launch_bounds__(kPassCTA, 1) pass_kernel(const PassArgs A) {
   const double fxyn = fxn * ifyn, fyxn = fyn * ifxn, fxyc = fxc * ifyc, fyxc = fyc * ifxc;
   const double iW = 1.0 / Wf;  // pixel index -> (u, v) without integer division
   const double dth[4] = {fxn - fxc, fyn - fyc, cxn - cxc, cyn - cyc};
-  int tau = 0;
+  int tau = 0, slot = 0;  // tile sequence number and its ring slot (tau mod NS)
 
   for (int sg = sg0; sg < sg1; ++sg) {
     const int fl = A.seg_frame[sg];
@@ -625,9 +625,9 @@ __global__ void __launch_bounds__(kPassCTA, 1) pass_kernel(const PassArgs A) {
     };
     prefetch(A.seg_t0[sg], tau & 1);
 
-    for (int tile = A.seg_t0[sg]; tile < A.seg_t1[sg]; ++tile, ++tau) {
+    for (int tile = A.seg_t0[sg]; tile < A.seg_t1[sg]; ++tile, ++tau, slot = slot + 1 == NS ? 0 : slot + 1) {
       const int pbase = tile * SUB;
-      const int tb = tau % NS;
+      const int tb = slot;
       double* const U = Ubuf + tb * ulen;  // this tile's ring slot
       double* const icv = icvb + tb * SUB;
       const float4* const fbuf = fbufb + (tau & 1) * KM * SUB;
