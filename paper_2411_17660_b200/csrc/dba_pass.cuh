@@ -289,7 +289,9 @@ __device__ __forceinline__ void gemm_shape(double (&macc)[QMAX][4][2], const dou
   }
 #pragma unroll 2
   for (int ks = 0; ks < nks; ++ks) {
-    const int pn = 4 * (ks + 1 < nks ? ks + 1 : ks);
+    // the last step prefetches the 4 padding columns of the slot (US = SUB + 4) and the
+    // shared words after its 1/C_p row: unused, and no per-step clamp
+    const int pn = 4 * (ks + 1);
     const double icn = icl[pn];
     double r0n[NI > 0 ? NI : 1], r1n[NI > 0 ? NI : 1], c0n[NC > 0 ? NC : 1], c1n[NC > 0 ? NC : 1];
 #pragma unroll
