@@ -10,8 +10,8 @@
 //     W_ab = S_ab Li_b^T,   S_ac -= W_ab W_cb^T,   L_ab = W_ab Li_b,   D_b^-1 = Li_b^T Li_b,
 // with a sliding window of BW+1 block rows resident in shared memory.  The symmetric
 // update W W^T is backward stable: the former L_ab S_cb^T form (explicit D_b^-1 from 3x3
-// adjugates) left the noisy-C3 step 4e-7 from the exact solution against 1e-10 for
-// LAPACK; this form matches LAPACK (numpy emulation).  The Cholesky pivot
+// adjugates) left the noisy-C3 step 5e-7 from the exact solution where LAPACK's Cholesky is
+// 1e-8; this form is 1.4e-8 (profiles/r02_solve_accuracy.txt).  The Cholesky pivot
 // test (every pivot > 0) is the SPD test.  Damping lambda is added to a diagonal block
 // when it becomes a pivot.
 //
@@ -23,11 +23,13 @@
 //    in parallel — half the chain length of the one-sided solve_kernel;
 //  * inside a chain one critical warp (warp 7: the arbiter issues higher warp ids
 //    first, and warp 3 on its scheduler only issues cp.async) forms the NEXT
-//    pivot while 6 warps apply the trailing update: one CTA barrier per step;
+//    pivot while 7 warps form the panels and apply the trailing update: one CTA
+//    barrier per step;
 //  * rows entering the window are copied with cp.async a step ahead;
 //  * back-substitution: w_b = D_b^-1 z_b for all b in parallel, then one warp
 //    sweeps without CTA barriers, folding x_b = w_b - sum L_ab^T x_a into the BW
-//    blocks above, factor rows streaming through an 8-deep cp.async ring.
+//    blocks above, factor rows streaming through a ring of bulk async copies (TMA
+//    engine) with full/empty mbarriers.
 // A non-SPD pivot aborts with status 1 (the host raises lambda).
 // The Cholesky pivots of the intrinsics Schur block give the A9 estimate.
 #pragma once
