@@ -638,7 +638,7 @@ __global__ void __launch_bounds__(kPassCTA, 1) pass_kernel(const PassArgs A) {
       for (int x = tid; x < SUB; x += kPassThreads) {
         const double pd = (double)(pbase + x);
         const double pv = floor((pd + 0.5) * iW), pu = fma(-pv, Wf, pd);  // exact: p < 2^40
-        qcs[x] = make_double2((pu - cxc) * ifxc, (pv - cyc) * ifyc);
+        if (A.backsub) qcs[x] = make_double2((pu - cxc) * ifxc, (pv - cyc) * ifyc);  // phase A only
         qns[x] = make_double2((pu - cxn) * ifxn, (pv - cyn) * ifyn);
       }
       nbar_sync(kBarGeo, kPassThreads);
