@@ -839,7 +839,8 @@ __global__ void __launch_bounds__(kPassCTA, 1) pass_kernel(const PassArgs A) {
         }
         // second extra column: A5 gauge c = C/d, or (scalefix) c = d (eta + alpha m), whose
         // E C^-1 c is the reduced system's exact row along the monocular scale direction
-        const double cx = A.scalefix ? dn * (A.eta + ap) : C * rcp64(dn);
+        // (only the gauge frame's and the scalefix rows are read by assemble_kernel)
+        const double cx = A.scalefix ? dn * (A.eta + ap) : gauge ? C * rcp64(dn) : 0.0;
         U[mu * US + pl] = gd;
         U[(mu + 1) * US + pl] = in ? cx : 0.0;
       }
